@@ -1,0 +1,158 @@
+"""One semi-implicit time step of the biofilm model.  Test infrastructure only.
+
+Splitting order (R1): Cahn-Hilliard -> nutrient -> momentum
+(Chorin projection: intermediate velocity, pressure Poisson, correction).
+PAPER.md §4 (lines 117-151) and Eq. 16 (lines 108-114).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import assemble as asm
+from . import explicit as ex
+from .krylov import bicgstab, cg, gmres
+from .params import Params
+
+
+@dataclass
+class State:
+    phi: np.ndarray        # phi_n^n       (ny, nx) cell centres
+    phi_prev: np.ndarray   # phi_n^{n-1}
+    c: np.ndarray          # nutrient c^n  cell centres
+    u: np.ndarray          # x-velocity on x-faces
+    v: np.ndarray          # y-velocity on y-faces (row 0 = bottom wall = 0)
+    p: np.ndarray          # pressure (paper's Eq. 20 variable, Δt absorbed; R15)
+    n: int = 0
+
+    def copy(self) -> "State":
+        return State(self.phi.copy(), self.phi_prev.copy(), self.c.copy(),
+                     self.u.copy(), self.v.copy(), self.p.copy(), self.n)
+
+
+@dataclass
+class StepInfo:
+    iters: dict = field(default_factory=dict)
+    div_max: float = 0.0
+
+
+def initial_state(fields: dict) -> State:
+    """phi^{-1} := phi^0 (first step extrapolates to phi* = phi^0, R5)."""
+    return State(phi=fields["phi"].copy(), phi_prev=fields["phi"].copy(),
+                 c=fields["c"].copy(), u=fields["u"].copy(),
+                 v=fields["v"].copy(), p=fields["p"].copy())
+
+
+def _solve_ch(A, b, x0, dinv, prm: Params):
+    if prm.ch_solver == "gmres":
+        return gmres(A, b, x0, dinv, prm.rtol, prm.maxit, prm.gmres_restart)
+    return bicgstab(A, b, x0, dinv, prm.rtol, prm.maxit)
+
+
+def ch_system(st: State, prm: Params):
+    """Linear system of the CH step (Eq. 16 4th line, Eq. 4-5; R5):
+      [I/dt + (G1/2) L_{M*} Δ_h] phi^{n+1}
+        = phi^n/dt + L_{M*}( F'(phi*) - (G1/2) Δ_h phi^n ) - div_h(phi* v^n) + g_n(phi*, c^n)
+    Returns (A, b, phi*)."""
+    ny, nx = st.phi.shape
+    phs = ex.phi_star(st.phi, st.phi_prev)
+    Mx, My = ex.mobility_faces(phs, prm.Lambda)
+    L_M = asm.flux_div(nx, ny, Mx, My)
+    Lap = asm.lap(nx, ny, "mirror")
+    A = asm.ch_matrix(nx, ny, prm.dt, prm.Gamma1, Mx, My)
+    mu_e = ex.fprime(phs, prm.Gamma2).ravel() - 0.5 * prm.Gamma1 * (Lap @ st.phi.ravel())
+    b = (st.phi.ravel() / prm.dt + L_M @ mu_e
+         - ex.advection(phs, st.u, st.v).ravel()
+         + ex.growth(phs, st.c, prm.eps, prm.mu, prm.Kc).ravel())
+    return A, b, phs
+
+
+def nutrient_system(st: State, phi1: np.ndarray, prm: Params):
+    """Nutrient step (Eq. 16 3rd line, Eq. 7; R11), Crank-Nicolson diffusion and
+    consumption, explicit advection of phi_s c at level n:
+      [diag(phi_s^{n+1}/dt + A/2 phi_n^{1/2}) - 1/2 L_K] c^{n+1}
+        = phi_s^n c^n/dt - div_h(phi_s^n c^n v^n) + 1/2 L_K c^n - A/2 phi_n^{1/2} c^n,
+    K = D_s phi_s^{1/2} on faces."""
+    ny, nx = st.phi.shape
+    ph = 0.5 * (st.phi + phi1)
+    sh = 1.0 - ph
+    s1 = 1.0 - phi1
+    s0 = 1.0 - st.phi
+    Kx = prm.Ds * 0.5 * (np.roll(sh, 1, axis=1) + sh)
+    Ky = np.zeros((ny + 1, nx))
+    Ky[1:ny] = prm.Ds * 0.5 * (sh[:-1] + sh[1:])
+    a_c = s1 / prm.dt + 0.5 * prm.A * ph
+    A = asm.nutrient_matrix(nx, ny, a_c, Kx, Ky)
+    L_K = asm.flux_div(nx, ny, Kx, Ky)
+    w = s0 * st.c
+    b = (w.ravel() / prm.dt - ex.advection(w, st.u, st.v).ravel()
+         + 0.5 * (L_K @ st.c.ravel()) - (0.5 * prm.A * ph * st.c).ravel())
+    return A, b
+
+
+def momentum_systems(st: State, phs: np.ndarray, prm: Params):
+    """Intermediate velocity (Eq. 19 with R restored, R6-R7), each component
+    divided through by nu = 1/(rho Re_a) to give an SPD system:
+      [a - 1/2 Δ_h^0] u* = a u^n + 1/2 Δ_h u^n + lid + (-(v^n·∇)u^n + R_x/rho)/nu,
+    a = 1/(nu dt); coefficients at phi* (R7)."""
+    ny, nx = st.phi.shape
+    hy = 1.0 / ny
+    Rx, Ry = ex.phase_stress(phs, prm.Gamma1)
+    fu = ex.face_phi_u(phs)
+    fv = ex.face_phi_v(phs)
+    rho_u = ex.density(fu, prm.rho_n, prm.rho_s)
+    rho_v = ex.density(fv, prm.rho_n, prm.rho_s)
+    nu_u = ex.inv_reynolds(fu, prm.Re_n, prm.Re_s) / rho_u
+    nu_v = ex.inv_reynolds(fv, prm.Re_n, prm.Re_s) / rho_v
+    a_u = 1.0 / (nu_u * prm.dt)
+    a_v = 1.0 / (nu_v * prm.dt)
+    Cu = ex.convective_u(st.u, st.v, prm.lid_u)
+    Cv = ex.convective_v(st.u, st.v)
+    bu = a_u * st.u + 0.5 * ex.lap_u_inhom(st.u, prm.lid_u) + (-Cu + Rx / rho_u) / nu_u
+    bu[-1] += prm.lid_u / hy ** 2          # implicit half of the lid ghost (R3)
+    bv = a_v * st.v + 0.5 * ex.lap_v(st.v) + (-Cv + Ry / rho_v) / nu_v
+    bv[0] = 0.0
+    Au = asm.u_matrix(nx, ny, a_u)
+    Av = asm.v_matrix(nx, ny, a_v)
+    return (Au, bu.ravel()), (Av, bv.ravel())
+
+
+def step(st: State, prm: Params) -> tuple[State, StepInfo]:
+    ny, nx = st.phi.shape
+    info = StepInfo()
+    # 1. Cahn-Hilliard (phi^{n+1}); initial guess phi* (R13)
+    A, b, phs = ch_system(st, prm)
+    dinv = 1.0 / A.diagonal()
+    phi1, info.iters["ch"] = _solve_ch(A, b, phs.ravel(), dinv, prm)
+    phi1 = phi1.reshape(ny, nx)
+    # 2. nutrient (c^{n+1}); guess c^n
+    A, b = nutrient_system(st, phi1, prm)
+    c1, info.iters["nutrient"] = cg(A, b, st.c.ravel(), 1.0 / A.diagonal(), prm.rtol, prm.maxit)
+    c1 = c1.reshape(ny, nx)
+    # 3. intermediate velocity (u*, v*); guesses u^n, v^n
+    (Au, bu), (Av, bv) = momentum_systems(st, phs, prm)
+    us, info.iters["u"] = cg(Au, bu, st.u.ravel(), 1.0 / Au.diagonal(), prm.rtol, prm.maxit)
+    vs, info.iters["v"] = cg(Av, bv, st.v.ravel(), 1.0 / Av.diagonal(), prm.rtol, prm.maxit)
+    us, vs = us.reshape(ny, nx), vs.reshape(ny, nx)
+    # 4. pressure Poisson (Eq. 20) with constant null space removed; guess p^n
+    bx, by = ex.pressure_faces(phi1, prm.rho_n, prm.rho_s)
+    Ap = asm.poisson_matrix(nx, ny, bx, by)
+    bp = ex.divergence(us, vs).ravel()
+    p1, info.iters["p"] = cg(Ap, bp, st.p.ravel(), 1.0 / Ap.diagonal(), prm.rtol, prm.maxit,
+                             nullspace=True)
+    p1 = p1.reshape(ny, nx)
+    # 5. projection (Eq. 21)
+    u1, v1 = ex.correct(us, vs, p1, bx, by)
+    info.div_max = float(np.abs(ex.divergence(u1, v1)).max())
+    new = State(phi=phi1, phi_prev=st.phi.copy(), c=c1, u=u1, v=v1, p=p1, n=st.n + 1)
+    return new, info
+
+
+def run(st: State, prm: Params, steps: int, callback=None) -> State:
+    for _ in range(steps):
+        st, info = step(st, prm)
+        if callback is not None:
+            callback(st, info)
+    return st
+
