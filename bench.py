@@ -1,0 +1,299 @@
+#!/usr/bin/env python
+"""Benchmark: time-steps/s of the biofilm time step (§4) at 4096^2 fp64
+on 1..8 B200 (BASELINE.json configs[3]), plus the HBM roofline of the dominant
+kernel, the oracle CPU baseline and an end-to-end (host buffers) number.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config 3] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (slab decomposition in y)
+
+One JSON line on rank 0.  A "step" is one full semi-implicit time step of the
+whole nx x ny domain (CH + nutrient + momentum + pressure solves, projection).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import CONFIGS, initial_fields  # noqa: E402
+
+METRIC = "time-steps/s at 4096^2 fp64 (HBM roofline of the dominant stencil kernel reported)"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------- CPU oracle leg
+def oracle_step_estimate(nx: int, ny: int, iters: dict, seed: int = 0, n_iter: int = 6):
+    """Bounded sample of the oracle at the FULL grid: assemble the pressure
+    Poisson system and run `n_iter` of its textbook CG iterations, timed; a step
+    is then estimated as 5 assemblies + sum over the 5 systems of (iterations
+    of this workload) x (per-iteration time), BiCGStab iterations counted
+    twice (two matvecs).  Returns (seconds per step, sample description)."""
+    import numpy as np
+    import oracle  # noqa: F401  (sets single-threaded BLAS)
+    from oracle import assemble as asm, explicit as ex
+    from oracle.krylov import NotConverged, cg
+    f = initial_fields(nx, ny, seed=seed)
+    t0 = time.perf_counter()
+    bx, by = ex.pressure_faces(f["phi"], 1.0, 1.0)
+    A = asm.poisson_matrix(nx, ny, bx, by)
+    b = np.random.default_rng(0).standard_normal(nx * ny)
+    t_asm = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    try:
+        cg(A, b, np.zeros(nx * ny), 1.0 / A.diagonal(), 1e-30, n_iter, nullspace=True)
+    except NotConverged:
+        pass
+    t_it = (time.perf_counter() - t1) / n_iter
+    total_it = sum(v * (2 if k == "ch" else 1) for k, v in iters.items())
+    est = 5 * t_asm + total_it * t_it
+    sample = (f"oracle at {nx}x{ny}: pressure-system assembly ({t_asm:.2f}s) + {n_iter} CG "
+              f"iterations ({t_it:.3f}s each) timed; step = 5 assemblies + {total_it} "
+              f"iterations (this workload's per-step Krylov counts)")
+    return est, sample, t_asm + n_iter * t_it
+
+
+def _iters_table(cfg_idx):
+    p = os.path.join(ROOT, "profiles", f"iters_config{cfg_idx}.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (there is no reference implementation),
+    timed on the host cores, each step a bounded sample of the workload."""
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    nx, ny = cfg["nx"], cfg["ny"]
+    iters = _iters_table(args.config) or {"ch": 2, "nutrient": 400, "u": 14000, "v": 14000, "p": 16000}
+    ests = []
+    sample = ""
+    for k in range(args.warmup + args.steps):
+        est, sample, _ = oracle_step_estimate(nx, ny, iters, n_iter=3)
+        if k >= args.warmup:
+            ests.append(est)
+    sec = sum(ests) / len(ests)
+    v = 1.0 / sec
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "time-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg["name"], "nx": nx, "ny": ny},
+            "cpu_baseline": {"value": v, "unit": "time-steps/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "time-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1811_11842_b200 import SimParams, Simulation, unique_id
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cfg = CONFIGS[args.config]
+    nx, ny = cfg["nx"], cfg["ny"]
+    sp = SimParams(dt=cfg["dt"], ch_solver=args.ch_solver)
+    sim = Simulation(nx, ny, sp, rank=rank, nranks=world, device=local_rank)
+    if world > 1:
+        obj = [unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        sim.comm_init(obj[0])
+    stream = torch.cuda.current_stream()
+    sim.set_stream(stream)
+    rows = (sim.row0, sim.row0 + sim.nrows)
+    f = initial_fields(nx, ny, seed=args.seed, rows=rows)
+    sim.set_fields(**f)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        sim.step(1)
+    barrier()
+    sim.reset_stats()
+    sim.enable_timing(args.timing_stride)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        sim.step(args.steps)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    sim.enable_timing(0)
+    st = sim.stats()
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = args.steps / (ms_max / 1e3)
+    ms_step = ms_max / args.steps
+
+    # roofline of the dominant kernel class (event-timed samples on this stream)
+    peak, peak_kind = _peaks()
+    dom = max(st["kernels"].items(), key=lambda kv: kv[1]["ms"] / max(kv[1]["timed"], 1) * kv[1]["launches"])
+    name, kd = dom
+    achieved = kd["bytes"] / (kd["ms"] / 1e3) / 1e9 if kd["ms"] > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get(name)
+    roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "peak_source": peak_kind,
+            "bytes_per_launch": kd["bytes"] / max(kd["timed"], 1),
+            "avg_launch_ms": kd["ms"] / max(kd["timed"], 1)}
+    per_class = {k: {"launches": v["launches"], "timed": v["timed"],
+                     "avg_ms": v["ms"] / max(v["timed"], 1),
+                     "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
+                 for k, v in st["kernels"].items() if v["launches"]}
+    iters_step = {k: v / args.steps for k, v in st["iters_total"].items()}
+
+    # end-to-end through the public API with host buffers (rank-local slab)
+    e2e = None
+    if not args.no_e2e:
+        host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory().numpy() for k, v in
+                sim.get_fields(("phi", "c", "u", "v", "p")).items()}
+        hprev = torch.from_numpy(sim.get_field("phi_prev")).pin_memory().numpy()
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            sim.set_fields(**host)
+            sim.set_field("phi_prev", hprev)
+            sim.step(1)
+            for k in host:
+                sim.get_field(k, host[k])
+            sim.get_field("phi_prev", hprev)
+        barrier()
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        nbytes = 6 * sim.nrows * nx * 8
+        e2e = {"value": e2e_steps / float(tt.item()), "unit": "time-steps/s",
+               "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        est, sample, wall = oracle_step_estimate(nx, ny, {k: int(round(v)) for k, v in iters_step.items()})
+        cpu = {"value": 1.0 / est, "unit": "time-steps/s", "cores": 1, "kind": "oracle",
+               "sample": sample, "sample_wall_s": round(wall, 2)}
+
+    if rank == 0:
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        line = {"metric": METRIC, "value": value, "unit": "time-steps/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": cfg["name"], "nx": nx, "ny": ny, "dt": cfg["dt"],
+                           "parallelism": f"slab-y x{world}", "ch_solver": args.ch_solver,
+                           "rtol": sp.rtol, "l2": "inputs larger than L2 (134 MB per field)",
+                           "krylov_iters_per_step": iters_step},
+                "roofline": roof, "kernels": per_class, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": st["launches"] * world, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ch-solver", default="bicgstab", choices=["bicgstab", "gmres"])
+    ap.add_argument("--timing-stride", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

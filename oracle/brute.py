@@ -196,3 +196,41 @@ def phase_stress(phis, Gamma1):
             ry[j, i] = -Gamma1 * ((txy(j, i + 1) - txy(j, i)) * nx
                                   + (tyy(j, i) - tyy(j - 1, i)) * ny)
     return rx, ry
+
+
+# ----------------------------------------------------- single-cell versions
+# For sampled checks at full size (4096^2): O(1) work per requested cell.
+def lap_at(s, j, i):
+    ny, nx = s.shape
+    c = S(s, j, i)
+    return ((S(s, j, i + 1) - 2 * c + S(s, j, i - 1)) * nx * nx
+            + (S(s, j + 1, i) - 2 * c + S(s, j - 1, i)) * ny * ny)
+
+
+def ch_apply_at(phis, x, j, i, dt, Gamma1, Lambda):
+    ny, nx = x.shape
+
+    def m(ja, ia, jb, ib):
+        return Lambda * max(0.0, 0.5 * (S(phis, ja, ia) + S(phis, jb, ib)))
+
+    wc = lap_at(x, j, i)
+    fe = m(j, i, j, i + 1) * (lap_at(x, j, i + 1) - wc)
+    fw = m(j, i - 1, j, i) * (wc - lap_at(x, j, i - 1))
+    fn = m(j, i, j + 1, i) * (lap_at(x, j + 1, i) - wc) if j + 1 < ny else 0.0
+    fs = m(j - 1, i, j, i) * (wc - lap_at(x, j - 1, i)) if j > 0 else 0.0
+    return S(x, j, i) / dt + 0.5 * Gamma1 * ((fe - fw) * nx * nx + (fn - fs) * ny * ny)
+
+
+def poisson_at(phi1, p, j, i, rho_n, rho_s):
+    ny, nx = p.shape
+
+    def beta(ja, ia, jb, ib):
+        m = 0.5 * (S(phi1, ja, ia) + S(phi1, jb, ib))
+        return 1.0 / (rho_s + m * (rho_n - rho_s))
+
+    c = S(p, j, i)
+    fe = beta(j, i, j, i + 1) * (S(p, j, i + 1) - c)
+    fw = beta(j, i - 1, j, i) * (c - S(p, j, i - 1))
+    fn = beta(j, i, j + 1, i) * (S(p, j + 1, i) - c) if j + 1 < ny else 0.0
+    fs = beta(j - 1, i, j, i) * (c - S(p, j - 1, i)) if j > 0 else 0.0
+    return -((fe - fw) * nx * nx + (fn - fs) * ny * ny)

@@ -1,0 +1,1045 @@
+// api.cu -- C ABI (include/ch_b200.h), handle/memory management, the Krylov
+// drivers (device-side scalars, host polls convergence once per chunk) and the
+// time-step orchestration of DESIGN.md §1.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "ch_b200.h"
+#include "comm.h"
+#include "common.cuh"
+#include "launch.h"
+
+using namespace chb;
+
+namespace {
+
+enum Arr {
+  A_PHI = 0, A_PHIP, A_C, A_U, A_V, A_P,   // state (pointer-swapped)
+  A_PHI1, A_C1, A_US, A_VS,                // next-level values
+  A_PHIS, A_DINV, A_B, A_CA, A_CW,         // phi*, CH Jacobi, rhs, coefficients
+  A_Z, A_PA, A_PB,                         // CG
+  A_R, A_RH, A_BP, A_BV, A_BS, A_BT,       // BiCGStab
+  A_TMP, A_TMP2,
+  A_N
+};
+
+constexpr int MAX_BLOCKS = 1 << 17;
+constexpr int NSC = CH_NSYS + 2;  // one KScal per system + apply + spare
+
+struct Slab {
+  Geom g;
+  double* a[A_N];
+  std::vector<double*> V;  // GMRES basis (m + 1 vectors) + work
+};
+
+struct Timer {
+  int stride = 0;
+  struct Rec {
+    int kc;
+    long iter;  // >= 0: Krylov iteration index of the launch (for useful filtering), -1: always
+    double bytes;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  long counter[CH_NKC] = {0};
+};
+
+}  // namespace
+
+struct ch_handle {
+  ch_grid grid;
+  ch_params prm;
+  int S = 1;                 // slabs in this process
+  int nslabs_total = 1;
+  std::vector<Slab> sl;
+  int row0 = 0, nrows = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  KScal* sc = nullptr;       // device [NSC]
+  KScal* sch = nullptr;      // pinned host [NSC]
+  double* part = nullptr;
+  unsigned int* ticket = nullptr;
+  double* tot = nullptr;     // [nslabs_total * 8]
+  double* tot_local = nullptr;
+  ch_stats stats;
+  std::string err;
+  Timer tm;
+  Comm* comm = nullptr;
+  size_t arr_elems = 0;
+  double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
+  double* gm_host = nullptr;  // pinned mirror
+};
+
+namespace {
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      h->err = std::string(#call) + ": " + cudaGetErrorName(e_) + " " +             \
+               cudaGetErrorString(e_);                                               \
+      return CH_ERR_CUDA;                                                            \
+    }                                                                                \
+  } while (0)
+
+#define TRY(x)               \
+  do {                       \
+    int s_ = (x);            \
+    if (s_ != CH_OK) return s_; \
+  } while (0)
+
+Phys phys(const ch_params& p) {
+  Phys ph;
+  ph.dt = p.dt; ph.Gamma1 = p.Gamma1; ph.Gamma2 = p.Gamma2; ph.Lambda = p.Lambda;
+  ph.mu = p.mu; ph.Kc = p.Kc; ph.eps = p.eps; ph.A = p.A; ph.Ds = p.Ds;
+  ph.Re_s = p.Re_s; ph.Re_n = p.Re_n; ph.rho_n = p.rho_n; ph.rho_s = p.rho_s;
+  ph.lid_u = p.lid_u;
+  return ph;
+}
+
+StateP state(const Slab& s) {
+  StateP p;
+  p.phi = s.a[A_PHI]; p.phip = s.a[A_PHIP]; p.c = s.a[A_C];
+  p.u = s.a[A_U]; p.v = s.a[A_V]; p.p = s.a[A_P];
+  return p;
+}
+
+int check_launch(ch_handle* h, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    h->err = std::string("launch ") + what + ": " + cudaGetErrorName(e) + " " +
+             cudaGetErrorString(e);
+    return CH_ERR_CUDA;
+  }
+  return CH_OK;
+}
+
+// ------------------------------------------------------------- timing
+cudaEvent_t ev_get(ch_handle* h) {
+  if (!h->tm.pool.empty()) {
+    cudaEvent_t e = h->tm.pool.back();
+    h->tm.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct KTime {
+  ch_handle* h;
+  int kc;
+  long iter;
+  double bytes;
+  bool on = false;
+  cudaEvent_t e0, e1;
+  // bytes: algorithmic bytes of ONE slab launch; the timed region covers all slabs
+  KTime(ch_handle* hh, int k, double b, long it = -1) : h(hh), kc(k), iter(it), bytes(b * hh->S) {
+    h->stats.launches += h->S;
+    h->stats.kc_launches[kc] += h->S;
+    if (h->tm.stride > 0 && (h->tm.counter[kc]++ % h->tm.stride) == 0) {
+      on = true;
+      e0 = ev_get(h);
+      e1 = ev_get(h);
+      cudaEventRecord(e0, h->st);
+    }
+  }
+  ~KTime() {
+    if (on) {
+      cudaEventRecord(e1, h->st);
+      h->tm.pending.push_back({kc, iter, bytes, e0, e1});
+    }
+  }
+};
+
+// Harvest timed launches.  Launches of Krylov iteration index > useful_iters
+// (no-op launches after convergence) are discarded.
+void harvest(ch_handle* h, long useful_iters) {
+  for (auto& r : h->tm.pending) {
+    if (r.iter < 0 || r.iter <= useful_iters) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, r.e0, r.e1) == cudaSuccess) {
+        h->stats.kc_ms[r.kc] += ms;
+        h->stats.kc_timed[r.kc] += 1;
+        h->stats.kc_bytes[r.kc] += r.bytes;
+      }
+    }
+    h->tm.pool.push_back(r.e0);
+    h->tm.pool.push_back(r.e1);
+  }
+  h->tm.pending.clear();
+}
+
+// ------------------------------------------------------ reductions / halos
+RedArgs rargs(ch_handle* h, int fin, int sys, int slab) {
+  RedArgs ra;
+  ra.part = h->part;
+  ra.ticket = h->ticket;
+  ra.tot = h->tot_local;
+  ra.sc = h->sc + sys;
+  ra.fc.rtol2 = h->prm.rtol * h->prm.rtol;
+  ra.fc.ncells = (double)h->grid.nx * (double)h->grid.ny;
+  ra.fin = fin;
+  ra.inline_fin = (h->nslabs_total == 1);
+  ra.slab = slab;
+  ra.pad = 0;
+  return ra;
+}
+
+// Combine slab totals (local slabs, then across ranks) and finalize.
+int fin_slabs(ch_handle* h, int fin, int sys, int K) {
+  if (h->nslabs_total == 1) return CH_OK;
+  const double* tot = h->tot_local;
+  if (h->comm) {
+    if (comm_allgather(h->comm, h->tot_local, h->tot, h->S * 8, h->st) != 0) {
+      h->err = "comm allgather failed";
+      return CH_ERR_COMM;
+    }
+    tot = h->tot;
+  }
+  RedArgs ra = rargs(h, fin, sys, 0);
+  launch_finalize_slabs(tot, h->nslabs_total, K, ra, h->st);
+  h->stats.launches += 1;
+  return check_launch(h, "finalize_slabs");
+}
+
+// Exchange `w` ghost rows of array `id` between neighbouring slabs.
+int halo(ch_handle* h, int id, int w) {
+  if (h->nslabs_total == 1) return CH_OK;
+  for (int s = 0; s + 1 < h->S; ++s) {
+    Slab& lo = h->sl[s];
+    Slab& hi = h->sl[s + 1];
+    const size_t pitch = lo.g.pitch;
+    // lo's top rows -> hi's bottom ghost rows
+    double* src = lo.a[id] + (size_t)(lo.g.nyl + GH - w) * pitch;
+    double* dst = hi.a[id] + (size_t)(GH - w) * pitch;
+    CK(cudaMemcpyAsync(dst, src, w * pitch * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    // hi's bottom rows -> lo's top ghost rows
+    src = hi.a[id] + (size_t)GH * pitch;
+    dst = lo.a[id] + (size_t)(lo.g.nyl + GH) * pitch;
+    CK(cudaMemcpyAsync(dst, src, w * pitch * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+  }
+  if (h->comm) {
+    std::vector<double*> bufs(h->S);
+    for (int s = 0; s < h->S; ++s) bufs[s] = h->sl[s].a[id];
+    const Slab& first = h->sl.front();
+    const Slab& last = h->sl.back();
+    if (comm_halo(h->comm, first.a[id], first.g.nyl, last.a[id], last.g.nyl, first.g.pitch, w,
+                  h->st) != 0) {
+      h->err = "comm halo failed";
+      return CH_ERR_COMM;
+    }
+  }
+  return CH_OK;
+}
+
+int copy_arr(ch_handle* h, int src, int dst) {
+  for (auto& s : h->sl)
+    CK(cudaMemcpyAsync(s.a[dst], s.a[src], h->arr_elems * sizeof(double),
+                       cudaMemcpyDeviceToDevice, h->st));
+  return CH_OK;
+}
+
+int poll(ch_handle* h, int sys) {
+  CK(cudaMemcpyAsync(h->sch + sys, h->sc + sys, sizeof(KScal), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return CH_OK;
+}
+
+int solve_status(ch_handle* h, int sys, const char* name) {
+  const KScal& s = h->sch[sys];
+  h->stats.iters_last[sys] = s.iter;
+  h->stats.iters_total[sys] += s.iter;
+  h->stats.resid_last[sys] = s.bb > 0 ? sqrt(s.rr / s.bb) : 0.0;
+  if (s.status == 1) {
+    h->err = std::string(name) + ": Krylov breakdown";
+    return CH_ERR_BREAKDOWN;
+  }
+  if (s.status == 2) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "%s: not converged in %d iterations (|r|/|b| = %.3e)", name,
+             s.iter, h->stats.resid_last[sys]);
+    h->err = buf;
+    return CH_ERR_NOT_CONVERGED;
+  }
+  return CH_OK;
+}
+
+int set_maxit(ch_handle* h, int sys) {
+  // maxit lives in the device scalars (read by the finalizers)
+  int m = h->prm.maxit;
+  CK(cudaMemcpyAsync(&h->sc[sys].maxit, &m, sizeof(int), cudaMemcpyHostToDevice, h->st));
+  return CH_OK;
+}
+
+// ------------------------------------------------------------------- CG
+OpDesc opdesc(ch_handle* h, int kind, const Slab& s) {
+  OpDesc d;
+  d.kind = kind;
+  d.strip = 16;
+  d.a = nullptr;
+  d.w = nullptr;
+  d.s = 1.0;
+  d.kscale = 1.0;
+  d.rho_n = h->prm.rho_n;
+  d.rho_s = h->prm.rho_s;
+  switch (kind) {
+    case OPK_POISSON_CONST: d.s = 1.0 / h->prm.rho_s; break;
+    case OPK_POISSON_VAR: d.w = s.a[A_PHI1]; break;
+    case OPK_NUTRIENT: d.a = s.a[A_CA]; d.w = s.a[A_CW]; d.s = 0.5; d.kscale = h->prm.Ds; break;
+    case OPK_MOM_U:
+    case OPK_MOM_V: d.a = s.a[A_CA]; d.s = 0.5; break;
+  }
+  return d;
+}
+
+int cg_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, int use_shift,
+             const char* name, int wid = -1) {
+  TRY(set_maxit(h, sys));
+  if (wid >= 0) TRY(halo(h, wid, 1));
+  TRY(halo(h, xid, 1));
+  {
+    KTime kt(h, CH_KC_CG_INIT, 40.0 * h->grid.nx * (double)h->nrows / h->S);
+    for (int s = 0; s < h->S; ++s) {
+      Slab& sl = h->sl[s];
+      launch_cg5_init(opdesc(h, kind, sl), sl.g, sl.a[xid], sl.a[bid], use_shift, sl.a[A_Z],
+                      rargs(h, FIN_CG_INIT, sys, s), h->st);
+    }
+  }
+  TRY(check_launch(h, "cg5_init"));
+  TRY(fin_slabs(h, FIN_CG_INIT, sys, 3));
+  TRY(halo(h, A_Z, 1));
+  const double cells = (double)h->grid.nx * (double)h->nrows / h->S;
+  long k = 1;
+  int chunk = 4;
+  for (;;) {
+    for (int it = 0; it < chunk; ++it, ++k) {
+      const int pold = (k & 1) ? A_PB : A_PA;
+      const int pnew = (k & 1) ? A_PA : A_PB;
+      {
+        KTime kt(h, CH_KC_CG_A, cg5_bytes_A(kind) * cells, k);
+        for (int s = 0; s < h->S; ++s) {
+          Slab& sl = h->sl[s];
+          launch_cg5_A(opdesc(h, kind, sl), sl.g, sl.a[A_Z], sl.a[pold], sl.a[pnew], sl.a[xid],
+                       k == 1, rargs(h, FIN_CG_A, sys, s), h->st);
+        }
+      }
+      TRY(fin_slabs(h, FIN_CG_A, sys, 1));
+      TRY(halo(h, pnew, 1));
+      {
+        KTime kt(h, CH_KC_CG_B, cg5_bytes_B(kind) * cells, k);
+        for (int s = 0; s < h->S; ++s) {
+          Slab& sl = h->sl[s];
+          launch_cg5_B(opdesc(h, kind, sl), sl.g, sl.a[pnew], sl.a[A_Z],
+                       rargs(h, FIN_CG_B, sys, s), h->st);
+        }
+      }
+      TRY(fin_slabs(h, FIN_CG_B, sys, 2));
+      TRY(halo(h, A_Z, 1));
+    }
+    TRY(check_launch(h, "cg5 iteration"));
+    TRY(poll(h, sys));
+    if (h->sch[sys].done) break;
+    if (chunk < 64) chunk *= 2;
+  }
+  const long K = h->sch[sys].iter;
+  const int plast = (K & 1) ? A_PA : A_PB;
+  {
+    KTime kt(h, CH_KC_VEC, 24.0 * cells);
+    for (int s = 0; s < h->S; ++s) {
+      Slab& sl = h->sl[s];
+      launch_cg5_finish(sl.g, sl.a[xid], sl.a[plast], nullspace, rargs(h, FIN_MEAN, sys, s),
+                        h->st);
+    }
+  }
+  TRY(check_launch(h, "cg5_finish"));
+  if (nullspace) TRY(fin_slabs(h, FIN_MEAN, sys, 1));
+  harvest(h, K);
+  return solve_status(h, sys, name);
+}
+
+// ------------------------------------------------------------ BiCGStab (CH)
+ChCoef chcoef(ch_handle* h, const Slab& s, bool precond) {
+  ChCoef c;
+  c.phis = s.a[A_PHIS];
+  c.dinv = precond ? s.a[A_DINV] : nullptr;
+  c.dt = h->prm.dt;
+  c.g1h = 0.5 * h->prm.Gamma1;
+  c.Lambda = h->prm.Lambda;
+  return c;
+}
+
+int bicgstab_solve(ch_handle* h, int sys, int xid, int bid) {
+  TRY(set_maxit(h, sys));
+  const double cells = (double)h->grid.nx * (double)h->nrows / h->S;
+  TRY(halo(h, xid, 2));
+  {
+    KTime kt(h, CH_KC_CH_APPLY, 24.0 * cells);
+    for (int s = 0; s < h->S; ++s) {
+      Slab& sl = h->sl[s];
+      launch_ch_apply(sl.g, chcoef(h, sl, false), sl.a[xid], sl.a[A_TMP], 0, nullptr, nullptr, 0,
+                      0, rargs(h, FIN_NONE, sys, s), h->st);
+    }
+  }
+  {
+    KTime kt(h, CH_KC_VEC, 32.0 * cells);
+    for (int s = 0; s < h->S; ++s) {
+      Slab& sl = h->sl[s];
+      launch_bi_init(sl.g, sl.a[A_TMP], sl.a[bid], sl.a[A_R], sl.a[A_RH],
+                     rargs(h, FIN_BI_INIT, sys, s), h->st);
+    }
+  }
+  TRY(fin_slabs(h, FIN_BI_INIT, sys, 2));
+  TRY(check_launch(h, "bicgstab init"));
+  long k = 1;
+  int chunk = 2;
+  for (;;) {
+    for (int it = 0; it < chunk; ++it, ++k) {
+      {
+        KTime kt(h, CH_KC_VEC, 32.0 * cells, k);
+        for (int s = 0; s < h->S; ++s) {
+          Slab& sl = h->sl[s];
+          launch_bi_p(sl.g, sl.a[A_R], sl.a[A_BP], sl.a[A_BV], k == 1, h->sc + sys, h->st);
+        }
+      }
+      TRY(halo(h, A_BP, 2));
+      {
+        KTime kt(h, CH_KC_CH_APPLY, 40.0 * cells, k);
+        for (int s = 0; s < h->S; ++s) {
+          Slab& sl = h->sl[s];
+          launch_ch_apply(sl.g, chcoef(h, sl, true), sl.a[A_BP], sl.a[A_BV], 1, sl.a[A_RH],
+                          nullptr, 1, 0, rargs(h, FIN_BI_ALPHA, sys, s), h->st);
+        }
+      }
+      TRY(fin_slabs(h, FIN_BI_ALPHA, sys, 1));
+      {
+        KTime kt(h, CH_KC_VEC, 24.0 * cells, k);
+        for (int s = 0; s < h->S; ++s) {
+          Slab& sl = h->sl[s];
+          launch_bi_s(sl.g, sl.a[A_R], sl.a[A_BV], sl.a[A_BS], rargs(h, FIN_BI_S, sys, s), h->st);
+        }
+      }
+      TRY(fin_slabs(h, FIN_BI_S, sys, 1));
+      TRY(halo(h, A_BS, 2));
+      {
+        KTime kt(h, CH_KC_CH_APPLY, 40.0 * cells, k);
+        for (int s = 0; s < h->S; ++s) {
+          Slab& sl = h->sl[s];
+          launch_ch_apply(sl.g, chcoef(h, sl, true), sl.a[A_BS], sl.a[A_BT], 2, sl.a[A_BS],
+                          nullptr, 1, 1, rargs(h, FIN_BI_OMEGA, sys, s), h->st);
+        }
+      }
+      TRY(fin_slabs(h, FIN_BI_OMEGA, sys, 2));
+      {
+        KTime kt(h, CH_KC_VEC, 64.0 * cells, k);
+        for (int s = 0; s < h->S; ++s) {
+          Slab& sl = h->sl[s];
+          launch_bi_xr(sl.g, sl.a[xid], sl.a[A_BP], sl.a[A_BS], sl.a[A_BT], sl.a[A_R],
+                       sl.a[A_RH], sl.a[A_DINV], rargs(h, FIN_BI_R, sys, s), h->st);
+        }
+      }
+      TRY(fin_slabs(h, FIN_BI_R, sys, 2));
+    }
+    TRY(check_launch(h, "bicgstab iteration"));
+    TRY(poll(h, sys));
+    if (h->sch[sys].done) break;
+    if (chunk < 32) chunk *= 2;
+  }
+  if (h->sch[sys].zero) {
+    for (auto& s : h->sl) CK(cudaMemsetAsync(s.a[xid], 0, h->arr_elems * sizeof(double), h->st));
+  }
+  harvest(h, h->sch[sys].iter);
+  return solve_status(h, sys, "cahn-hilliard");
+}
+
+int gmres_solve(ch_handle* h, int sys, int xid, int bid);  // below
+
+// ------------------------------------------------------------- one step
+int step_once(ch_handle* h) {
+  const Phys ph = phys(h->prm);
+  const double cells = (double)h->grid.nx * (double)h->nrows / h->S;
+  // 1. Cahn-Hilliard
+  TRY(halo(h, A_PHI, 2));
+  TRY(halo(h, A_PHIP, 2));
+  TRY(halo(h, A_U, 1));
+  TRY(halo(h, A_V, 1));
+  TRY(halo(h, A_C, 1));
+  {
+    KTime kt(h, CH_KC_RHS, 72.0 * cells);
+    for (auto& s : h->sl) launch_ch_rhs(s.g, ph, state(s), s.a[A_PHIS], s.a[A_DINV], s.a[A_B], h->st);
+  }
+  TRY(check_launch(h, "ch_rhs"));
+  TRY(halo(h, A_PHIS, 2));
+  TRY(halo(h, A_DINV, 2));
+  TRY(copy_arr(h, A_PHIS, A_PHI1));
+  if (h->prm.ch_solver == CH_SOLVER_GMRES)
+    TRY(gmres_solve(h, CH_SYS_CH, A_PHI1, A_B));
+  else
+    TRY(bicgstab_solve(h, CH_SYS_CH, A_PHI1, A_B));
+  // 2. nutrient
+  TRY(halo(h, A_PHI1, 1));
+  {
+    KTime kt(h, CH_KC_RHS, 64.0 * cells);
+    for (auto& s : h->sl)
+      launch_nut_rhs(s.g, ph, state(s), s.a[A_PHI1], s.a[A_CA], s.a[A_CW], s.a[A_B], h->st);
+  }
+  TRY(check_launch(h, "nut_rhs"));
+  TRY(copy_arr(h, A_C, A_C1));
+  TRY(cg_solve(h, CH_SYS_NUTRIENT, OPK_NUTRIENT, A_C1, A_B, 0, 0, "nutrient", A_CW));
+  // 3. intermediate velocity
+  {
+    KTime kt(h, CH_KC_RHS, 40.0 * cells);
+    for (auto& s : h->sl) launch_mom_rhs_u(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_B], h->st);
+  }
+  TRY(check_launch(h, "mom_rhs_u"));
+  TRY(copy_arr(h, A_U, A_US));
+  TRY(cg_solve(h, CH_SYS_U, OPK_MOM_U, A_US, A_B, 0, 0, "momentum-u"));
+  {
+    KTime kt(h, CH_KC_RHS, 40.0 * cells);
+    for (auto& s : h->sl) launch_mom_rhs_v(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_B], h->st);
+  }
+  TRY(check_launch(h, "mom_rhs_v"));
+  TRY(copy_arr(h, A_V, A_VS));
+  TRY(cg_solve(h, CH_SYS_V, OPK_MOM_V, A_VS, A_B, 0, 0, "momentum-v"));
+  // 4. pressure Poisson with the constant null space
+  TRY(halo(h, A_US, 1));
+  TRY(halo(h, A_VS, 1));
+  {
+    KTime kt(h, CH_KC_RHS, 24.0 * cells);
+    for (int s = 0; s < h->S; ++s) {
+      Slab& sl = h->sl[s];
+      launch_div(sl.g, sl.a[A_US], sl.a[A_VS], sl.a[A_B], rargs(h, FIN_MEAN, CH_SYS_P, s), h->st);
+    }
+  }
+  TRY(check_launch(h, "div"));
+  TRY(fin_slabs(h, FIN_MEAN, CH_SYS_P, 1));
+  const int pk = (h->prm.rho_n == h->prm.rho_s) ? OPK_POISSON_CONST : OPK_POISSON_VAR;
+  TRY(cg_solve(h, CH_SYS_P, pk, A_P, A_B, 1, 1, "pressure", pk == OPK_POISSON_VAR ? A_PHI1 : -1));
+  {
+    KTime kt(h, CH_KC_VEC, 16.0 * cells);
+    for (auto& s : h->sl) launch_sub_mean(s.g, s.a[A_P], h->sc + CH_SYS_P, h->st);
+  }
+  // 5. projection
+  TRY(halo(h, A_P, 1));
+  {
+    KTime kt(h, CH_KC_RHS, 56.0 * cells);
+    for (auto& s : h->sl)
+      launch_project(s.g, ph, s.a[A_PHI1], s.a[A_US], s.a[A_VS], s.a[A_P], s.a[A_U], s.a[A_V], h->st);
+  }
+  TRY(check_launch(h, "project"));
+  // rotate time levels
+  for (auto& s : h->sl) {
+    std::swap(s.a[A_PHIP], s.a[A_PHI]);   // phi_prev <- phi^n
+    std::swap(s.a[A_PHI], s.a[A_PHI1]);   // phi <- phi^{n+1}
+    std::swap(s.a[A_C], s.a[A_C1]);
+  }
+  harvest(h, -1);
+  h->stats.steps += 1;
+  return CH_OK;
+}
+
+// ------------------------------------------------------------ field copies
+int field_arr(int field) {
+  switch (field) {
+    case CH_FIELD_PHI: return A_PHI;
+    case CH_FIELD_PHI_PREV: return A_PHIP;
+    case CH_FIELD_C: return A_C;
+    case CH_FIELD_U: return A_U;
+    case CH_FIELD_V: return A_V;
+    case CH_FIELD_P: return A_P;
+  }
+  return -1;
+}
+
+// Copy a user (nrows x nx, ld = nx) array into internal array `id` of all slabs.
+int put(ch_handle* h, int id, const double* src, int where) {
+  const cudaMemcpyKind k = where == CH_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  for (auto& s : h->sl) {
+    const double* sp = src + (size_t)(s.g.j0 - h->row0) * h->grid.nx;
+    double* dp = s.a[id] + (size_t)GH * s.g.pitch;
+    CK(cudaMemcpy2DAsync(dp, s.g.pitch * sizeof(double), sp, h->grid.nx * sizeof(double),
+                         h->grid.nx * sizeof(double), s.g.nyl, k, h->st));
+  }
+  if (where != CH_DEVICE) CK(cudaStreamSynchronize(h->st));
+  return CH_OK;
+}
+
+int get(ch_handle* h, int id, double* dst, int where) {
+  const cudaMemcpyKind k = where == CH_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  for (auto& s : h->sl) {
+    double* dp = dst + (size_t)(s.g.j0 - h->row0) * h->grid.nx;
+    const double* sp = s.a[id] + (size_t)GH * s.g.pitch;
+    CK(cudaMemcpy2DAsync(dp, h->grid.nx * sizeof(double), sp, s.g.pitch * sizeof(double),
+                         h->grid.nx * sizeof(double), s.g.nyl, k, h->st));
+  }
+  if (where != CH_DEVICE) CK(cudaStreamSynchronize(h->st));
+  return CH_OK;
+}
+
+int zero_vrow0(ch_handle* h) {
+  if (h->row0 == 0) {
+    Slab& s = h->sl.front();
+    CK(cudaMemsetAsync(s.a[A_V] + (size_t)GH * s.g.pitch, 0, s.g.pitch * sizeof(double), h->st));
+  }
+  return CH_OK;
+}
+
+}  // namespace
+
+// ======================================================================
+// GMRES(m) with right Jacobi preconditioning (PAPER.md:238 KSPGMRES +
+// PCJACOBI).  Arnoldi by classical Gram-Schmidt with one
+// re-orthogonalisation (CGS2): every basis vector is read twice per step in
+// fused multi-dot / multi-axpy sweeps instead of j+1 dependent passes.  The
+// (m+1) x m Hessenberg least-squares problem (Givens rotations) is tiny and
+// runs on the host from the reduced coefficients.
+namespace {
+
+int gm_dots(ch_handle* h, int k, int wvec, std::vector<double>& out) {
+  // out[i] = (V_i, V_wvec) for i < k, summed over slabs in slab order (and ranks)
+  out.assign(k, 0.0);
+  for (auto& s : h->sl) {
+    launch_gm_dots(s.g, s.V.data(), k, s.V[wvec], h->gm_dev, h->part, h->ticket, h->st);
+    CK(cudaMemcpyAsync(h->gm_host, h->gm_dev, k * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    for (int i = 0; i < k; ++i) out[i] += h->gm_host[i];
+  }
+  h->stats.launches += h->S;
+  h->stats.kc_launches[CH_KC_GMRES] += h->S;
+  if (h->comm)
+    for (int i = 0; i < k; ++i) out[i] = comm_allreduce_host(h->comm, out[i]);
+  return check_launch(h, "gm_dots");
+}
+
+int gm_set_coef(ch_handle* h, const double* v, int k) {
+  CK(cudaMemcpyAsync(h->gm_dev + 96, v, k * sizeof(double), cudaMemcpyHostToDevice, h->st));
+  return CH_OK;
+}
+
+int gmres_solve(ch_handle* h, int sys, int xid, int bid) {
+  const int m = std::max(1, std::min(64, (int)h->prm.gmres_restart));
+  const double cells = (double)h->grid.nx * (double)h->nrows / h->S;
+  for (auto& s : h->sl)
+    while ((int)s.V.size() < m + 1) {
+      double* p = nullptr;
+      CK(cudaMalloc(&p, h->arr_elems * sizeof(double)));
+      CK(cudaMemsetAsync(p, 0, h->arr_elems * sizeof(double), h->st));
+      s.V.push_back(p);
+    }
+  KScal& hs = h->sch[sys];
+  memset(&hs, 0, sizeof(KScal));
+  // ||b||^2: stage b in V[0]
+  for (auto& s : h->sl)
+    CK(cudaMemcpyAsync(s.V[0], s.a[bid], h->arr_elems * sizeof(double), cudaMemcpyDeviceToDevice,
+                       h->st));
+  std::vector<double> t;
+  TRY(gm_dots(h, 1, 0, t));
+  hs.bb = t[0];
+  if (hs.bb == 0.0) {
+    for (auto& s : h->sl) CK(cudaMemsetAsync(s.a[xid], 0, h->arr_elems * sizeof(double), h->st));
+    return solve_status(h, sys, "cahn-hilliard (gmres)");
+  }
+  const double tol = h->prm.rtol * sqrt(hs.bb);
+  long total = 0;
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gv(m + 1), y(m);
+  for (;;) {
+    // V0 = b - A x
+    TRY(halo(h, xid, 2));
+    {
+      KTime kt(h, CH_KC_CH_APPLY, 24.0 * cells);
+      for (int s = 0; s < h->S; ++s) {
+        Slab& sl = h->sl[s];
+        launch_ch_apply(sl.g, chcoef(h, sl, false), sl.a[xid], sl.a[A_TMP], 0, nullptr, nullptr,
+                        0, 0, rargs(h, FIN_NONE, sys, s), h->st);
+        launch_gm_residual(sl.g, sl.a[A_TMP], sl.a[bid], sl.V[0], h->st);
+      }
+    }
+    TRY(check_launch(h, "gmres residual"));
+    TRY(gm_dots(h, 1, 0, t));
+    const double beta = sqrt(t[0]);
+    if (beta <= tol) {
+      hs.rr = t[0];
+      break;
+    }
+    const double ib = 1.0 / beta;
+    TRY(gm_set_coef(h, &ib, 1));
+    for (auto& s : h->sl) launch_gm_scale(s.g, s.V[0], h->gm_dev + 96, h->st);
+    std::fill(H.begin(), H.end(), 0.0);
+    std::fill(gv.begin(), gv.end(), 0.0);
+    gv[0] = beta;
+    int k = 0;
+    bool conv = false;
+    for (int j = 0; j < m; ++j) {
+      total++;
+      // w = A D^{-1} V_j -> V_{j+1}   (multi-slab: V_j staged in TMP2 for its halo)
+      if (h->nslabs_total > 1) {
+        for (auto& s : h->sl)
+          CK(cudaMemcpyAsync(s.a[A_TMP2], s.V[j], h->arr_elems * sizeof(double),
+                             cudaMemcpyDeviceToDevice, h->st));
+        TRY(halo(h, A_TMP2, 2));
+      }
+      {
+        KTime kt(h, CH_KC_CH_APPLY, 32.0 * cells, total);
+        for (int s = 0; s < h->S; ++s) {
+          Slab& sl = h->sl[s];
+          const double* src = h->nslabs_total > 1 ? sl.a[A_TMP2] : sl.V[j];
+          launch_ch_apply(sl.g, chcoef(h, sl, true), src, sl.V[j + 1], 0, nullptr, nullptr, 0, 0,
+                          rargs(h, FIN_NONE, sys, s), h->st);
+        }
+      }
+      // CGS2: h = V^T w; w -= V h; twice
+      std::vector<double> hc(j + 1, 0.0), hp;
+      for (int pass = 0; pass < 2; ++pass) {
+        TRY(gm_dots(h, j + 1, j + 1, hp));
+        TRY(gm_set_coef(h, hp.data(), j + 1));
+        {
+          KTime kt(h, CH_KC_GMRES, 8.0 * (j + 3) * cells, total);
+          for (auto& s : h->sl)
+            launch_gm_axpy_multi(s.g, s.V.data(), j + 1, h->gm_dev + 96, s.V[j + 1], h->st);
+        }
+        for (int i = 0; i <= j; ++i) hc[i] += hp[i];
+      }
+      // ||w||: self dot of V_{j+1}
+      {
+        std::vector<double> all;
+        // (V_i, V_{j+1}) for i <= j+1, last entry is the squared norm
+        TRY(gm_dots(h, j + 2, j + 1, all));
+        H[(size_t)(j + 1) * m + j] = sqrt(all[j + 1]);
+      }
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hc[i];
+      const double hn = H[(size_t)(j + 1) * m + j];
+      if (hn != 0.0) {
+        const double ihn = 1.0 / hn;
+        TRY(gm_set_coef(h, &ihn, 1));
+        for (auto& s : h->sl) launch_gm_scale(s.g, s.V[j + 1], h->gm_dev + 96, h->st);
+      }
+      for (int i = 0; i < j; ++i) {
+        const double a0 = H[(size_t)i * m + j], a1 = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * a0 + sn[i] * a1;
+        H[(size_t)(i + 1) * m + j] = -sn[i] * a0 + cs[i] * a1;
+      }
+      const double den = hypot(H[(size_t)j * m + j], hn);
+      cs[j] = H[(size_t)j * m + j] / den;
+      sn[j] = hn / den;
+      H[(size_t)j * m + j] = den;
+      H[(size_t)(j + 1) * m + j] = 0.0;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      k = j + 1;
+      if (fabs(gv[j + 1]) <= tol || total >= h->prm.maxit) {
+        conv = fabs(gv[j + 1]) <= tol;
+        break;
+      }
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double acc = gv[i];
+      for (int l = i + 1; l < k; ++l) acc -= H[(size_t)i * m + l] * y[l];
+      y[i] = acc / H[(size_t)i * m + i];
+    }
+    TRY(gm_set_coef(h, y.data(), k));
+    {
+      KTime kt(h, CH_KC_GMRES, 8.0 * (k + 3) * cells);
+      for (auto& s : h->sl)
+        launch_gm_update_x(s.g, s.V.data(), k, h->gm_dev + 96, s.a[A_DINV], s.a[xid], h->st);
+    }
+    TRY(check_launch(h, "gmres update"));
+    hs.rr = gv[k] * gv[k];
+    if (conv) break;
+    if (total >= h->prm.maxit) {
+      hs.status = 2;
+      break;
+    }
+  }
+  hs.iter = (int)total;
+  CK(cudaStreamSynchronize(h->st));
+  harvest(h, -1);
+  return solve_status(h, sys, "cahn-hilliard (gmres)");
+}
+
+}  // namespace
+
+// ======================================================================
+// C ABI
+extern "C" {
+
+int ch_abi_version(void) { return CH_ABI_VERSION; }
+
+const char* ch_last_error(const ch_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+static void destroy_mem(ch_handle* h) {
+  for (auto& s : h->sl) {
+    for (int i = 0; i < A_N; ++i)
+      if (s.a[i]) cudaFree(s.a[i]);
+    for (double* p : s.V) cudaFree(p);
+  }
+  h->sl.clear();
+  if (h->sc) cudaFree(h->sc);
+  if (h->sch) cudaFreeHost(h->sch);
+  if (h->part) cudaFree(h->part);
+  if (h->ticket) cudaFree(h->ticket);
+  if (h->tot) cudaFree(h->tot);
+  if (h->tot_local) cudaFree(h->tot_local);
+  if (h->gm_dev) cudaFree(h->gm_dev);
+  if (h->gm_host) cudaFreeHost(h->gm_host);
+  for (auto& r : h->tm.pending) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  for (auto e : h->tm.pool) cudaEventDestroy(e);
+  h->tm.pending.clear();
+  h->tm.pool.clear();
+}
+
+ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) {
+  auto fail = [&](int code, ch_handle* h, const char* msg) -> ch_handle* {
+    if (status) *status = code;
+    if (h) {
+      fprintf(stderr, "ch_create: %s %s\n", msg, h->err.c_str());
+      destroy_mem(h);
+      delete h;
+    } else {
+      fprintf(stderr, "ch_create: %s\n", msg);
+    }
+    return nullptr;
+  };
+  if (!grid || !params) return fail(CH_ERR_ARG, nullptr, "null argument");
+  const ch_grid G = *grid;
+  if (G.nx < 4 || G.ny < 4 || G.nranks < 1 || G.rank < 0 || G.rank >= G.nranks)
+    return fail(CH_ERR_ARG, nullptr, "bad grid (need nx, ny >= 4, 0 <= rank < nranks)");
+  const int S = G.virtual_slabs < 1 ? 1 : G.virtual_slabs;
+  const int total = G.nranks * S;
+  if (G.ny < 2 * total) return fail(CH_ERR_ARG, nullptr, "too many slabs for ny (>= 2 rows each)");
+  if (!(params->dt > 0) || !(params->rtol > 0) || params->maxit < 1)
+    return fail(CH_ERR_ARG, nullptr, "bad params (dt > 0, rtol > 0, maxit >= 1)");
+  if (cudaSetDevice(G.device) != cudaSuccess) return fail(CH_ERR_CUDA, nullptr, "cudaSetDevice");
+  ch_handle* h = new ch_handle();
+  h->grid = G;
+  h->prm = *params;
+  h->S = S;
+  h->nslabs_total = total;
+  memset(&h->stats, 0, sizeof(ch_stats));
+  // rows: balanced split of ny over `total` slabs (first ny % total get one more)
+  const int base = G.ny / total, rem = G.ny % total;
+  auto slab_row0 = [&](int k) { return k * base + std::min(k, rem); };
+  const int pitch = ((G.nx + 31) / 32) * 32;
+  h->row0 = slab_row0(G.rank * S);
+  h->nrows = slab_row0(G.rank * S + S) - h->row0;
+  int maxrows = 0;
+  for (int s = 0; s < S; ++s) {
+    const int k = G.rank * S + s;
+    maxrows = std::max(maxrows, slab_row0(k + 1) - slab_row0(k));
+  }
+  h->arr_elems = (size_t)(maxrows + 2 * GH) * pitch;
+  h->sl.resize(S);
+  for (int s = 0; s < S; ++s) {
+    Slab& sl = h->sl[s];
+    const int k = G.rank * S + s;
+    sl.g.nx = G.nx;
+    sl.g.ny = G.ny;
+    sl.g.j0 = slab_row0(k);
+    sl.g.nyl = slab_row0(k + 1) - sl.g.j0;
+    sl.g.pitch = pitch;
+    sl.g.pad = 0;
+    sl.g.hx = 1.0 / G.nx;
+    sl.g.hy = 1.0 / G.ny;
+    sl.g.ihx = (double)G.nx;
+    sl.g.ihy = (double)G.ny;
+    sl.g.ihx2 = (double)G.nx * G.nx;
+    sl.g.ihy2 = (double)G.ny * G.ny;
+    for (int i = 0; i < A_N; ++i) sl.a[i] = nullptr;
+    for (int i = 0; i < A_N; ++i) {
+      if (cudaMalloc(&sl.a[i], h->arr_elems * sizeof(double)) != cudaSuccess)
+        return fail(CH_ERR_CUDA, h, "cudaMalloc (out of device memory?)");
+      cudaMemset(sl.a[i], 0, h->arr_elems * sizeof(double));
+    }
+  }
+  if (cudaMalloc(&h->sc, NSC * sizeof(KScal)) != cudaSuccess ||
+      cudaMallocHost(&h->sch, NSC * sizeof(KScal)) != cudaSuccess ||
+      cudaMalloc(&h->part, (size_t)MAX_BLOCKS * 8 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&h->ticket, sizeof(unsigned int)) != cudaSuccess ||
+      cudaMalloc(&h->tot, (size_t)total * 8 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&h->tot_local, (size_t)total * 8 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&h->gm_dev, 192 * sizeof(double)) != cudaSuccess ||
+      cudaMallocHost(&h->gm_host, 192 * sizeof(double)) != cudaSuccess)
+    return fail(CH_ERR_CUDA, h, "cudaMalloc (scalars)");
+  cudaMemset(h->sc, 0, NSC * sizeof(KScal));
+  memset(h->sch, 0, NSC * sizeof(KScal));
+  cudaMemset(h->ticket, 0, sizeof(unsigned int));
+  h->st = nullptr;
+  // c = 1 initially
+  {
+    std::vector<double> ones((size_t)h->arr_elems, 1.0);
+    for (auto& s : h->sl) cudaMemcpy(s.a[A_C], ones.data(), h->arr_elems * sizeof(double),
+                                     cudaMemcpyHostToDevice);
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(CH_ERR_CUDA, h, "init sync");
+  if (status) *status = CH_OK;
+  return h;
+}
+
+int ch_comm_unique_id(void* id_out, size_t len) { return comm_unique_id(id_out, len); }
+
+int ch_comm_init(ch_handle* h, const void* id, size_t len) {
+  if (!h) return CH_ERR_ARG;
+  if (h->grid.nranks == 1) return CH_OK;
+  h->comm = comm_create(id, len, h->grid.rank, h->grid.nranks, h->grid.device, &h->err);
+  return h->comm ? CH_OK : CH_ERR_COMM;
+}
+
+int ch_local_rows(const ch_handle* h, int32_t* row0, int32_t* nrows) {
+  if (!h) return CH_ERR_ARG;
+  if (row0) *row0 = h->row0;
+  if (nrows) *nrows = h->nrows;
+  return CH_OK;
+}
+
+int ch_set_stream(ch_handle* h, void* stream) {
+  if (!h) return CH_ERR_ARG;
+  h->st = (cudaStream_t)stream;
+  return CH_OK;
+}
+
+int ch_set_field(ch_handle* h, int field, const double* src, int where) {
+  if (!h || !src) return CH_ERR_ARG;
+  const int id = field_arr(field);
+  if (id < 0) {
+    h->err = "bad field id";
+    return CH_ERR_ARG;
+  }
+  TRY(put(h, id, src, where));
+  if (field == CH_FIELD_V) TRY(zero_vrow0(h));
+  return CH_OK;
+}
+
+int ch_set_fields(ch_handle* h, const double* phi, const double* c, const double* u,
+                  const double* v, const double* p, int where) {
+  if (!h) return CH_ERR_ARG;
+  if (phi) {
+    TRY(put(h, A_PHI, phi, where));
+    TRY(copy_arr(h, A_PHI, A_PHIP));
+  }
+  if (c) TRY(put(h, A_C, c, where));
+  if (u) TRY(put(h, A_U, u, where));
+  if (v) {
+    TRY(put(h, A_V, v, where));
+    TRY(zero_vrow0(h));
+  }
+  if (p) TRY(put(h, A_P, p, where));
+  if (where != CH_DEVICE) CK(cudaStreamSynchronize(h->st));
+  return CH_OK;
+}
+
+int ch_get_field(ch_handle* h, int field, double* dst, int where) {
+  if (!h || !dst) return CH_ERR_ARG;
+  const int id = field_arr(field);
+  if (id < 0) {
+    h->err = "bad field id";
+    return CH_ERR_ARG;
+  }
+  return get(h, id, dst, where);
+}
+
+int ch_get_fields(ch_handle* h, double* phi, double* c, double* u, double* v, double* p,
+                  int where) {
+  if (!h) return CH_ERR_ARG;
+  if (phi) TRY(get(h, A_PHI, phi, where));
+  if (c) TRY(get(h, A_C, c, where));
+  if (u) TRY(get(h, A_U, u, where));
+  if (v) TRY(get(h, A_V, v, where));
+  if (p) TRY(get(h, A_P, p, where));
+  return CH_OK;
+}
+
+int ch_step(ch_handle* h, int nsteps) {
+  if (!h || nsteps < 0) return CH_ERR_ARG;
+  for (int n = 0; n < nsteps; ++n) TRY(step_once(h));
+  return CH_OK;
+}
+
+int ch_apply_operator(ch_handle* h, int op, const double* x, double* y, int where) {
+  if (!h || !x || !y) return CH_ERR_ARG;
+  const Phys ph = phys(h->prm);
+  TRY(halo(h, A_PHI, 2));
+  TRY(halo(h, A_PHIP, 2));
+  TRY(halo(h, A_U, 1));
+  TRY(halo(h, A_V, 1));
+  TRY(halo(h, A_C, 1));
+  for (auto& s : h->sl) launch_ch_rhs(s.g, ph, state(s), s.a[A_PHIS], s.a[A_DINV], s.a[A_TMP2], h->st);
+  TRY(halo(h, A_PHIS, 2));
+  TRY(put(h, A_TMP, x, where));
+  switch (op) {
+    case CH_OP_CH:
+      TRY(halo(h, A_TMP, 2));
+      for (int s = 0; s < h->S; ++s) {
+        Slab& sl = h->sl[s];
+        launch_ch_apply(sl.g, chcoef(h, sl, false), sl.a[A_TMP], sl.a[A_B], 0, nullptr, nullptr,
+                        0, 0, rargs(h, FIN_NONE, CH_NSYS, s), h->st);
+      }
+      break;
+    case CH_OP_POISSON: {
+      TRY(copy_arr(h, A_PHI, A_PHI1));
+      TRY(halo(h, A_TMP, 1));
+      const int pk = (h->prm.rho_n == h->prm.rho_s) ? OPK_POISSON_CONST : OPK_POISSON_VAR;
+      for (auto& s : h->sl) launch_op5_apply(opdesc(h, pk, s), s.g, s.a[A_TMP], s.a[A_B], h->st);
+      break;
+    }
+    case CH_OP_MOM_U:
+    case CH_OP_MOM_V: {
+      TRY(halo(h, A_TMP, 1));
+      for (auto& s : h->sl) {
+        if (op == CH_OP_MOM_U)
+          launch_mom_rhs_u(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_TMP2], h->st);
+        else
+          launch_mom_rhs_v(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_TMP2], h->st);
+        launch_op5_apply(opdesc(h, op == CH_OP_MOM_U ? OPK_MOM_U : OPK_MOM_V, s), s.g, s.a[A_TMP],
+                         s.a[A_B], h->st);
+      }
+      break;
+    }
+    default:
+      h->err = "bad operator id";
+      return CH_ERR_ARG;
+  }
+  TRY(check_launch(h, "apply_operator"));
+  TRY(get(h, A_B, y, where));
+  if (where == CH_DEVICE) CK(cudaStreamSynchronize(h->st));
+  return CH_OK;
+}
+
+int ch_get_stats(const ch_handle* h, ch_stats* out) {
+  if (!h || !out) return CH_ERR_ARG;
+  *out = h->stats;
+  return CH_OK;
+}
+
+int ch_reset_stats(ch_handle* h) {
+  if (!h) return CH_ERR_ARG;
+  const int64_t steps = h->stats.steps;
+  memset(&h->stats, 0, sizeof(ch_stats));
+  h->stats.steps = steps;
+  return CH_OK;
+}
+
+int ch_enable_timing(ch_handle* h, int stride) {
+  if (!h || stride < 0) return CH_ERR_ARG;
+  h->tm.stride = stride;
+  return CH_OK;
+}
+
+void ch_destroy(ch_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->grid.device);
+  if (h->st) cudaStreamSynchronize(h->st);
+  cudaDeviceSynchronize();
+  if (h->comm) comm_destroy(h->comm);
+  destroy_mem(h);
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,22 @@
+// comm.h -- inter-process transport for the slab decomposition (internal).
+// NCCL is loaded at run time (dlopen "libnccl.so.2", the library torch already
+// uses) only when a handle has nranks > 1, so single-GPU use has no NCCL
+// dependency.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include <string>
+
+struct Comm;
+
+int comm_unique_id(void* out, size_t len);
+Comm* comm_create(const void* id, size_t len, int rank, int nranks, int device, std::string* err);
+// recv[r * count .. (r+1) * count) = send of rank r (rank-ordered, deterministic)
+int comm_allgather(Comm* c, const double* send, double* recv, size_t count, cudaStream_t st);
+// y-slab halo: the first local slab exchanges its bottom w rows with rank-1,
+// the last local slab its top w rows with rank+1 (non-periodic in y).
+int comm_halo(Comm* c, double* first_base, int first_nyl, double* last_base, int last_nyl,
+              int pitch, int w, cudaStream_t st);
+double comm_allreduce_host(Comm* c, double v);
+void comm_destroy(Comm* c);

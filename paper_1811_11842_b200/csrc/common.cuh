@@ -1,0 +1,255 @@
+// common.cuh -- device-side building blocks shared by all kernels of the
+// B200 hot path (slab geometry, wall ghost rules applied at read time,
+// deterministic block reductions with a last-block finalizer, Krylov scalars).
+//
+// DESIGN.md §2 (discretisation) and §5 (layout).  Nothing here is shared with
+// oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace chb {
+
+constexpr int GH = 2;               // ghost rows stored below and above a slab
+constexpr unsigned FULL = 0xffffffffu;
+
+// Ghost rules of the unknown / field (R2-R4).
+enum Bc : int {
+  BC_MIRROR = 0,  // cell-centred scalar: s[-1-k] = s[k], s[ny+k] = s[ny-1-k]
+  BC_ODD = 1,     // u on x-faces, homogeneous: u[-1-k] = -u[k] (lid handled by RHS)
+  BC_VFACE = 2    // v on y-faces: v = 0 on the wall faces j = 0 and j = ny
+};
+
+// Geometry of one slab (rows [j0, j0+nyl) of the global nx x ny grid).
+struct Geom {
+  int nx, ny;       // global cells
+  int j0, nyl;      // first global row, local row count
+  int pitch;        // doubles per stored row (>= nx, multiple of 32)
+  int pad;
+  double hx, hy, ihx, ihy, ihx2, ihy2;
+};
+
+__device__ __forceinline__ size_t off(const Geom& g, int gj, int c) {
+  return (size_t)(gj - g.j0 + GH) * (size_t)g.pitch + (size_t)c;
+}
+
+// Load value of a field with ghost rule BC at global row gj (|overhang| <= 2),
+// column c in [0, nx).  Rows outside the slab but inside the domain come from
+// the stored ghost rows (filled by the halo exchange).
+template <int BC>
+__device__ __forceinline__ double ldf(const double* __restrict__ a, const Geom& g, int gj, int c) {
+  if (BC == BC_VFACE) {
+    if (gj <= 0 || gj >= g.ny) return 0.0;
+    return a[off(g, gj, c)];
+  }
+  if (gj < 0) {
+    double v = a[off(g, -1 - gj, c)];
+    return BC == BC_ODD ? -v : v;
+  }
+  if (gj >= g.ny) {
+    double v = a[off(g, 2 * g.ny - 1 - gj, c)];
+    return BC == BC_ODD ? -v : v;
+  }
+  return a[off(g, gj, c)];
+}
+
+// u (state) with the inhomogeneous wall values: no-slip below, lid above.
+__device__ __forceinline__ double ld_u_lid(const double* __restrict__ u, const Geom& g, int gj,
+                                           int c, double lid) {
+  if (gj < 0) return -u[off(g, -1 - gj, c)];
+  if (gj >= g.ny) return 2.0 * lid - u[off(g, 2 * g.ny - 1 - gj, c)];
+  return u[off(g, gj, c)];
+}
+
+__device__ __forceinline__ int wrapc(int c, int nx) { return c < 0 ? c + nx : (c >= nx ? c - nx : c); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// ----------------------------------------------------------- Krylov scalars
+struct KScal {
+  double rho, rho_prev, alpha, beta, omega;
+  double bb, tol2, rr, last;      // ||b||^2, rtol^2 ||b||^2, ||r||^2, scratch
+  double mean;                    // mean used by null-space projections
+  double aux[6];
+  int iter, done, status, half;   // status: 0 ok, 1 breakdown, 2 maxit
+  int zero, maxit, pad0, pad1;
+};
+
+enum Fin : int {
+  FIN_NONE = 0,
+  FIN_CG_INIT,     // [bb, rz, rr]
+  FIN_CG_A,        // [pq]
+  FIN_CG_B,        // [rz, rr]
+  FIN_BI_INIT,     // [bb, rr]           (rhat = r  => rho = rr)
+  FIN_BI_ALPHA,    // [rhat.v]
+  FIN_BI_S,        // [s.s]
+  FIN_BI_OMEGA,    // [t.s, t.t]
+  FIN_BI_R,        // [r.r, rhat.r]
+  FIN_MEAN,        // [sum]  -> mean = sum / ncells
+  FIN_STORE        // [v...] -> aux[k] = v[k]
+};
+
+struct FinCtx {
+  double rtol2;
+  double ncells;
+};
+
+__device__ __forceinline__ bool bad(double x) { return !(x == x) || x == 0.0; }
+
+__device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx& fc) {
+  switch (fin) {
+    case FIN_CG_INIT: {
+      s->bb = t[0];
+      s->tol2 = fc.rtol2 * t[0];
+      s->rho = t[1];
+      s->rr = t[2];
+      s->iter = 0;
+      s->status = 0;
+      s->half = 0;
+      s->zero = (t[0] == 0.0);
+      s->done = s->zero || (t[2] <= s->tol2);
+      break;
+    }
+    case FIN_CG_A: {
+      if (!(t[0] > 0.0) || !(s->rho == s->rho)) { s->status = 1; s->done = 1; break; }
+      s->alpha = s->rho / t[0];
+      break;
+    }
+    case FIN_CG_B: {
+      s->iter += 1;
+      s->rr = t[1];
+      if (t[1] <= s->tol2) { s->done = 1; break; }
+      if (s->iter >= s->maxit) { s->status = 2; s->done = 1; break; }
+      s->beta = t[0] / s->rho;
+      s->rho = t[0];
+      break;
+    }
+    case FIN_BI_INIT: {
+      s->bb = t[0];
+      s->tol2 = fc.rtol2 * t[0];
+      s->rr = t[1];
+      s->rho = t[1];
+      s->rho_prev = 1.0;
+      s->alpha = 1.0;
+      s->omega = 1.0;
+      s->iter = 0;
+      s->status = 0;
+      s->half = 0;
+      s->zero = (t[0] == 0.0);
+      s->done = s->zero || (t[1] <= s->tol2);
+      break;
+    }
+    case FIN_BI_ALPHA: {
+      if (bad(t[0])) { s->status = 1; s->done = 1; break; }
+      s->alpha = s->rho / t[0];
+      break;
+    }
+    case FIN_BI_S: {
+      s->half = (t[0] <= s->tol2);
+      if (s->half) s->rr = t[0];
+      break;
+    }
+    case FIN_BI_OMEGA: {
+      if (s->half) break;
+      if (bad(t[1])) { s->status = 1; s->done = 1; break; }
+      s->omega = t[0] / t[1];
+      break;
+    }
+    case FIN_BI_R: {
+      s->iter += 1;
+      if (s->half) { s->done = 1; break; }
+      s->rr = t[0];
+      if (t[0] <= s->tol2) { s->done = 1; break; }
+      if (s->iter >= s->maxit) { s->status = 2; s->done = 1; break; }
+      if (t[1] == 0.0 || !(t[1] == t[1]) || s->omega == 0.0) { s->status = 1; s->done = 1; break; }
+      s->rho_prev = s->rho;
+      s->rho = t[1];
+      break;
+    }
+    case FIN_MEAN: {
+      s->mean = t[0] / fc.ncells;
+      break;
+    }
+    case FIN_STORE: {
+      for (int k = 0; k < 6; ++k) s->aux[k] = t[k];
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+// Reduction plumbing: every block writes K partial sums; the last block to
+// finish (atomic ticket) sums the partials in fixed block order (deterministic)
+// and either finalizes inline (single slab, single rank) or stores the slab
+// total for a later cross-slab finalize.
+struct RedArgs {
+  double* part;          // [nblocks * 8]
+  unsigned int* ticket;  // zeroed; reset by the last block
+  double* tot;           // [nslabs_total * 8] slab totals (when !inline_fin)
+  KScal* sc;
+  FinCtx fc;
+  int fin;
+  int inline_fin;
+  int slab;              // index of this slab in tot
+  int pad;
+};
+
+template <int K>
+__device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedArgs& ra) {
+  __shared__ double sm[32][K > 0 ? K : 1];
+  __shared__ int am_last;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  const int nw = (blockDim.x * blockDim.y + 31) >> 5;
+  const int bid = blockIdx.x + blockIdx.y * gridDim.x;
+  const int nb = gridDim.x * gridDim.y;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) sm[wid][k] = v[k];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double t = lane < nw ? sm[lane][k] : 0.0;
+      t = warp_sum(t);
+      if (lane == 0) ra.part[(size_t)bid * 8 + k] = t;
+    }
+    if (lane == 0) {
+      __threadfence();
+      unsigned prev = atomicAdd(ra.ticket, 1u);
+      am_last = (prev == (unsigned)(nb - 1));
+    }
+  }
+  __syncthreads();
+  if (!am_last || wid != 0) return;
+  __threadfence();
+  double res[K > 0 ? K : 1];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double t = 0.0;
+    for (int b = lane; b < nb; b += 32) t += __ldcg(ra.part + (size_t)b * 8 + k);
+    res[k] = warp_sum(t);
+  }
+  if (lane == 0) {
+    *ra.ticket = 0u;
+    if (ra.inline_fin) {
+      finalize(ra.fin, res, ra.sc, ra.fc);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) ra.tot[ra.slab * 8 + k] = res[k];
+    }
+  }
+}
+
+// Cross-slab finalize: sums slab totals in slab order, then finalizes.
+__global__ void k_finalize_slabs(const double* tot, int nslabs, int K, RedArgs ra);
+
+}  // namespace chb

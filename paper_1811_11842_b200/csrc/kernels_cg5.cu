@@ -1,0 +1,408 @@
+// kernels_cg5.cu -- the 5-point symmetric operator family and its fused
+// Jacobi-preconditioned CG half-iterations (the hot path of every step:
+// pressure Poisson, Eq. 20; intermediate velocity, Eq. 19; nutrient, Eq. 16).
+//
+//   y = a x + s * sum_faces k_f (x - x_nb) / h_f^2
+//
+// Operator instances (OpKind):
+//   POISSON_CONST  a = 0, s = 1, k = 1                      (rho_n == rho_s)
+//   POISSON_VAR    a = 0, s = 1, k = 1/rho(face mean phi^{n+1})
+//   NUTRIENT       a = a_c[], s = 1/2, k = D_s * face mean(phi_s^{1/2})
+//   MOM_U          a = a_u[], s = 1/2, k = 1, odd-reflection walls
+//   MOM_V          a = a_v[], s = 1/2, k = 1, Dirichlet wall faces, row 0 = identity
+//
+// Memory plan per CG iteration (z-form CG: z = D^{-1} r is stored, r = d z is
+// re-formed in registers, so D^{-1} is never needed at a neighbour):
+//   A: read z, p_old, x (+coef);  write p, x;   reduce (p, Ap)         40 B/cell
+//   B: read p, z (+coef);         write z;      reduce (r, z), (r, r)  24 B/cell
+// Each thread owns one column and marches down a strip of rows keeping the
+// three-row window in registers; x-neighbours come from warp shuffles (edge
+// lanes and the periodic seam reload through L1).
+#include "common.cuh"
+#include "launch.h"
+
+namespace chb {
+
+struct Op5 {
+  const double* a;   // diagonal coefficient at the unknown's location (AM = 1)
+  const double* w;   // cell-centred coefficient source (KM = 1, 2)
+  double s;          // face-term scale
+  double kscale;     // KM = 1: k = kscale * mean(w)
+  double rho_n, rho_s;
+};
+
+template <int KM>
+__device__ __forceinline__ double kface(const Op5& op, double w1, double w2) {
+  if (KM == 0) return 1.0;
+  const double m = 0.5 * (w1 + w2);
+  if (KM == 1) return op.kscale * m;
+  return 1.0 / (op.rho_s + m * (op.rho_n - op.rho_s));
+}
+
+// y = (A x) at one cell and its diagonal d.  Neighbour values are already
+// ghost-folded for the unknown's BC; w values are mirror-folded.
+template <int BC, int AM, int KM>
+__device__ __forceinline__ void eval5(const Op5& op, const Geom& g, int gj, double ac, double wc,
+                                      double ww, double we, double ws, double wn, double xc,
+                                      double xw, double xe, double xs, double xn, double& y,
+                                      double& d) {
+  if (BC == BC_VFACE && gj == 0) {  // wall row: identity
+    y = xc;
+    d = 1.0;
+    return;
+  }
+  const double kE = kface<KM>(op, wc, we), kW = kface<KM>(op, ww, wc);
+  const double kN = kface<KM>(op, wc, wn), kS = kface<KM>(op, ws, wc);
+  double fS = 1.0, fN = 1.0;
+  if (BC == BC_MIRROR) {
+    fS = (gj == 0) ? 0.0 : 1.0;
+    fN = (gj == g.ny - 1) ? 0.0 : 1.0;
+  } else if (BC == BC_ODD) {
+    fS = (gj == 0) ? 2.0 : 1.0;
+    fN = (gj == g.ny - 1) ? 2.0 : 1.0;
+  }
+  const double a = AM ? ac : 0.0;
+  y = a * xc + op.s * ((kE * (xc - xe) + kW * (xc - xw)) * g.ihx2 +
+                       (kN * (xc - xn) + kS * (xc - xs)) * g.ihy2);
+  d = a + op.s * ((kE + kW) * g.ihx2 + (fN * kN + fS * kS) * g.ihy2);
+}
+
+// ---------------------------------------------------------------------------
+// Column-marching helpers.  All threads of a block run the same row loop.
+struct Col {
+  int c, cc, cw, ce, lane;
+  bool act, needW, needE;
+  __device__ __forceinline__ Col(const Geom& g) {
+    lane = threadIdx.x & 31;
+    c = blockIdx.x * blockDim.x + threadIdx.x;
+    act = c < g.nx;
+    cc = act ? c : g.nx - 1;
+    cw = wrapc(cc - 1, g.nx);
+    ce = wrapc(cc + 1, g.nx);
+    needW = (lane == 0) || (c == 0);
+    needE = (lane == 31) || (c + 1 >= g.nx);
+  }
+};
+
+#define CHB_SHFL_W(v) __shfl_up_sync(FULL, (v), 1)
+#define CHB_SHFL_E(v) __shfl_down_sync(FULL, (v), 1)
+
+// ------------------------------------------------------------------ CG init
+// r = (b - shift) - A x;  z = r / d;  reduce ||b - shift||^2, (r, z), (r, r)
+template <int BC, int AM, int KM>
+__global__ void __launch_bounds__(128) k_cg5_init(Geom g, Op5 op, const double* __restrict__ x,
+                                                  const double* __restrict__ b, int use_shift,
+                                                  double* __restrict__ z, int strip, RedArgs ra) {
+  const double shift = use_shift ? ra.sc->mean : 0.0;
+  Col col(g);
+  const int jl0 = blockIdx.y * strip, jl1 = min(jl0 + strip, g.nyl);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  int gj = g.j0 + jl0;
+  double xm = ldf<BC>(x, g, gj - 1, col.cc), x0 = ldf<BC>(x, g, gj, col.cc);
+  double wm = 0.0, w0 = 0.0;
+  if (KM) {
+    wm = ldf<BC_MIRROR>(op.w, g, gj - 1, col.cc);
+    w0 = ldf<BC_MIRROR>(op.w, g, gj, col.cc);
+  }
+  for (int jl = jl0; jl < jl1; ++jl, ++gj) {
+    const double xp = ldf<BC>(x, g, gj + 1, col.cc);
+    double xw = CHB_SHFL_W(x0), xe = CHB_SHFL_E(x0);
+    if (col.needW) xw = ldf<BC>(x, g, gj, col.cw);
+    if (col.needE) xe = ldf<BC>(x, g, gj, col.ce);
+    double wp = 0.0, ww = 0.0, we = 0.0;
+    if (KM) {
+      wp = ldf<BC_MIRROR>(op.w, g, gj + 1, col.cc);
+      ww = CHB_SHFL_W(w0);
+      we = CHB_SHFL_E(w0);
+      if (col.needW) ww = ldf<BC_MIRROR>(op.w, g, gj, col.cw);
+      if (col.needE) we = ldf<BC_MIRROR>(op.w, g, gj, col.ce);
+    }
+    const double ac = AM ? op.a[off(g, gj, col.cc)] : 0.0;
+    double y, d;
+    eval5<BC, AM, KM>(op, g, gj, ac, w0, ww, we, wm, wp, x0, xw, xe, xm, xp, y, d);
+    if (col.act) {
+      const size_t o = off(g, gj, col.c);
+      const double bc = b[o] - ((BC == BC_VFACE && gj == 0) ? 0.0 : shift);
+      const double r = bc - y;
+      const double zz = r / d;
+      z[o] = zz;
+      s0 += bc * bc;
+      s1 += r * zz;
+      s2 += r * r;
+    }
+    xm = x0;
+    x0 = xp;
+    wm = w0;
+    w0 = wp;
+  }
+  double v[3] = {s0, s1, s2};
+  block_reduce_finalize<3>(v, ra);
+}
+
+// --------------------------------------------------------------- CG half A
+// p = z + beta p_old (p = z on the first iteration);  x += alpha_prev p_old;
+// q = A p;  reduce (p, q)  -> alpha = rho / (p, q)
+template <int BC, int AM, int KM>
+__global__ void __launch_bounds__(128) k_cg5_A(Geom g, Op5 op, const double* __restrict__ z,
+                                               const double* __restrict__ po,
+                                               double* __restrict__ pn, double* __restrict__ x,
+                                               int first, int strip, RedArgs ra) {
+  if (ra.sc->done) return;
+  const double beta = first ? 0.0 : ra.sc->beta;
+  const double alpha = first ? 0.0 : ra.sc->alpha;
+  Col col(g);
+  const int jl0 = blockIdx.y * strip, jl1 = min(jl0 + strip, g.nyl);
+  double acc = 0.0;
+  int gj = g.j0 + jl0;
+  auto P = [&](int r, int cidx) -> double {
+    double v = ldf<BC>(z, g, r, cidx);
+    if (!first) v += beta * ldf<BC>(po, g, r, cidx);
+    return v;
+  };
+  double pm = P(gj - 1, col.cc), p0 = P(gj, col.cc);
+  double wm = 0.0, w0 = 0.0;
+  if (KM) {
+    wm = ldf<BC_MIRROR>(op.w, g, gj - 1, col.cc);
+    w0 = ldf<BC_MIRROR>(op.w, g, gj, col.cc);
+  }
+  for (int jl = jl0; jl < jl1; ++jl, ++gj) {
+    const double pp = P(gj + 1, col.cc);
+    double pw = CHB_SHFL_W(p0), pe = CHB_SHFL_E(p0);
+    if (col.needW) pw = P(gj, col.cw);
+    if (col.needE) pe = P(gj, col.ce);
+    double wp = 0.0, ww = 0.0, we = 0.0;
+    if (KM) {
+      wp = ldf<BC_MIRROR>(op.w, g, gj + 1, col.cc);
+      ww = CHB_SHFL_W(w0);
+      we = CHB_SHFL_E(w0);
+      if (col.needW) ww = ldf<BC_MIRROR>(op.w, g, gj, col.cw);
+      if (col.needE) we = ldf<BC_MIRROR>(op.w, g, gj, col.ce);
+    }
+    const double ac = AM ? op.a[off(g, gj, col.cc)] : 0.0;
+    double y, d;
+    eval5<BC, AM, KM>(op, g, gj, ac, w0, ww, we, wm, wp, p0, pw, pe, pm, pp, y, d);
+    if (col.act) {
+      const size_t o = off(g, gj, col.c);
+      pn[o] = p0;
+      if (!first) x[o] += alpha * po[o];
+      acc += p0 * y;
+    }
+    pm = p0;
+    p0 = pp;
+    wm = w0;
+    w0 = wp;
+  }
+  double v[1] = {acc};
+  block_reduce_finalize<1>(v, ra);
+}
+
+// --------------------------------------------------------------- CG half B
+// r = d z - alpha A p;  z = r / d;  reduce (r, z), (r, r)
+template <int BC, int AM, int KM>
+__global__ void __launch_bounds__(128) k_cg5_B(Geom g, Op5 op, const double* __restrict__ p,
+                                               double* __restrict__ z, int strip, RedArgs ra) {
+  if (ra.sc->done) return;
+  const double alpha = ra.sc->alpha;
+  Col col(g);
+  const int jl0 = blockIdx.y * strip, jl1 = min(jl0 + strip, g.nyl);
+  double s0 = 0.0, s1 = 0.0;
+  int gj = g.j0 + jl0;
+  double pm = ldf<BC>(p, g, gj - 1, col.cc), p0 = ldf<BC>(p, g, gj, col.cc);
+  double wm = 0.0, w0 = 0.0;
+  if (KM) {
+    wm = ldf<BC_MIRROR>(op.w, g, gj - 1, col.cc);
+    w0 = ldf<BC_MIRROR>(op.w, g, gj, col.cc);
+  }
+  for (int jl = jl0; jl < jl1; ++jl, ++gj) {
+    const double pp = ldf<BC>(p, g, gj + 1, col.cc);
+    double pw = CHB_SHFL_W(p0), pe = CHB_SHFL_E(p0);
+    if (col.needW) pw = ldf<BC>(p, g, gj, col.cw);
+    if (col.needE) pe = ldf<BC>(p, g, gj, col.ce);
+    double wp = 0.0, ww = 0.0, we = 0.0;
+    if (KM) {
+      wp = ldf<BC_MIRROR>(op.w, g, gj + 1, col.cc);
+      ww = CHB_SHFL_W(w0);
+      we = CHB_SHFL_E(w0);
+      if (col.needW) ww = ldf<BC_MIRROR>(op.w, g, gj, col.cw);
+      if (col.needE) we = ldf<BC_MIRROR>(op.w, g, gj, col.ce);
+    }
+    const double ac = AM ? op.a[off(g, gj, col.cc)] : 0.0;
+    double y, d;
+    eval5<BC, AM, KM>(op, g, gj, ac, w0, ww, we, wm, wp, p0, pw, pe, pm, pp, y, d);
+    if (col.act) {
+      const size_t o = off(g, gj, col.c);
+      const double r = d * z[o] - alpha * y;
+      const double zz = r / d;
+      z[o] = zz;
+      s0 += r * zz;
+      s1 += r * r;
+    }
+    pm = p0;
+    p0 = pp;
+    wm = w0;
+    w0 = wp;
+  }
+  double v[2] = {s0, s1};
+  block_reduce_finalize<2>(v, ra);
+}
+
+// --------------------------------------------------------------- plain apply
+template <int BC, int AM, int KM>
+__global__ void __launch_bounds__(128) k_op5_apply(Geom g, Op5 op, const double* __restrict__ x,
+                                                   double* __restrict__ yout, int strip) {
+  Col col(g);
+  const int jl0 = blockIdx.y * strip, jl1 = min(jl0 + strip, g.nyl);
+  int gj = g.j0 + jl0;
+  double xm = ldf<BC>(x, g, gj - 1, col.cc), x0 = ldf<BC>(x, g, gj, col.cc);
+  double wm = 0.0, w0 = 0.0;
+  if (KM) {
+    wm = ldf<BC_MIRROR>(op.w, g, gj - 1, col.cc);
+    w0 = ldf<BC_MIRROR>(op.w, g, gj, col.cc);
+  }
+  for (int jl = jl0; jl < jl1; ++jl, ++gj) {
+    const double xp = ldf<BC>(x, g, gj + 1, col.cc);
+    double xw = CHB_SHFL_W(x0), xe = CHB_SHFL_E(x0);
+    if (col.needW) xw = ldf<BC>(x, g, gj, col.cw);
+    if (col.needE) xe = ldf<BC>(x, g, gj, col.ce);
+    double wp = 0.0, ww = 0.0, we = 0.0;
+    if (KM) {
+      wp = ldf<BC_MIRROR>(op.w, g, gj + 1, col.cc);
+      ww = CHB_SHFL_W(w0);
+      we = CHB_SHFL_E(w0);
+      if (col.needW) ww = ldf<BC_MIRROR>(op.w, g, gj, col.cw);
+      if (col.needE) we = ldf<BC_MIRROR>(op.w, g, gj, col.ce);
+    }
+    const double ac = AM ? op.a[off(g, gj, col.cc)] : 0.0;
+    double y, d;
+    eval5<BC, AM, KM>(op, g, gj, ac, w0, ww, we, wm, wp, x0, xw, xe, xm, xp, y, d);
+    if (col.act) yout[off(g, gj, col.c)] = y;
+    xm = x0;
+    x0 = xp;
+    wm = w0;
+    w0 = wp;
+  }
+}
+
+// ---------------------------------------------------------------- CG finish
+// x += alpha p (last iteration's update, deferred by the A kernel), or x = 0
+// when b = 0; optional reduction of sum(x) for the null-space projection.
+__global__ void __launch_bounds__(256) k_cg5_finish(Geom g, double* __restrict__ x,
+                                                    const double* __restrict__ p, int nullspace,
+                                                    RedArgs ra) {
+  const KScal* sc = ra.sc;
+  const int zero = sc->zero;
+  const int upd = (sc->iter >= 1) && !zero && sc->status == 0;
+  const double alpha = sc->alpha;
+  double acc = 0.0;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int jl = blockIdx.y; jl < g.nyl; jl += gridDim.y) {
+    if (c < g.nx) {
+      const size_t o = off(g, g.j0 + jl, c);
+      double v = zero ? 0.0 : x[o];
+      if (upd) v += alpha * p[o];
+      x[o] = v;
+      acc += v;
+    }
+  }
+  if (nullspace) {
+    double v[1] = {acc};
+    block_reduce_finalize<1>(v, ra);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sub_mean(Geom g, double* __restrict__ x, const KScal* sc) {
+  const double m = sc->mean;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int jl = blockIdx.y; jl < g.nyl; jl += gridDim.y)
+    if (c < g.nx) x[off(g, g.j0 + jl, c)] -= m;
+}
+
+__global__ void k_finalize_slabs(const double* tot, int nslabs, int K, RedArgs ra) {
+  if (threadIdx.x != 0) return;
+  double t[8];
+  for (int k = 0; k < K; ++k) {
+    double s = 0.0;
+    for (int i = 0; i < nslabs; ++i) s += tot[i * 8 + k];
+    t[k] = s;
+  }
+  finalize(ra.fin, t, ra.sc, ra.fc);
+}
+
+// ============================================================== launchers
+static Op5 make_op(const OpDesc& d) {
+  Op5 o;
+  o.a = d.a;
+  o.w = d.w;
+  o.s = d.s;
+  o.kscale = d.kscale;
+  o.rho_n = d.rho_n;
+  o.rho_s = d.rho_s;
+  return o;
+}
+
+static dim3 grid5(const Geom& g, int strip) {
+  return dim3((g.nx + 127) / 128, (g.nyl + strip - 1) / strip);
+}
+
+#define CHB_DISPATCH(KIND, CALL)                                        \
+  switch (KIND) {                                                       \
+    case OPK_POISSON_CONST: { constexpr int BC = BC_MIRROR, AM = 0, KM = 0; CALL; } break; \
+    case OPK_POISSON_VAR:   { constexpr int BC = BC_MIRROR, AM = 0, KM = 2; CALL; } break; \
+    case OPK_NUTRIENT:      { constexpr int BC = BC_MIRROR, AM = 1, KM = 1; CALL; } break; \
+    case OPK_MOM_U:         { constexpr int BC = BC_ODD,    AM = 1, KM = 0; CALL; } break; \
+    case OPK_MOM_V:         { constexpr int BC = BC_VFACE,  AM = 1, KM = 0; CALL; } break; \
+    default: break;                                                     \
+  }
+
+void launch_cg5_init(const OpDesc& d, const Geom& g, const double* x, const double* b,
+                     int use_shift, double* z, const RedArgs& ra, cudaStream_t st) {
+  const Op5 op = make_op(d);
+  const int strip = d.strip;
+  CHB_DISPATCH(d.kind, (k_cg5_init<BC, AM, KM><<<grid5(g, strip), 128, 0, st>>>(
+                           g, op, x, b, use_shift, z, strip, ra)));
+}
+
+void launch_cg5_A(const OpDesc& d, const Geom& g, const double* z, const double* po, double* pn,
+                  double* x, int first, const RedArgs& ra, cudaStream_t st) {
+  const Op5 op = make_op(d);
+  const int strip = d.strip;
+  CHB_DISPATCH(d.kind, (k_cg5_A<BC, AM, KM><<<grid5(g, strip), 128, 0, st>>>(
+                           g, op, z, po, pn, x, first, strip, ra)));
+}
+
+void launch_cg5_B(const OpDesc& d, const Geom& g, const double* p, double* z, const RedArgs& ra,
+                  cudaStream_t st) {
+  const Op5 op = make_op(d);
+  const int strip = d.strip;
+  CHB_DISPATCH(d.kind, (k_cg5_B<BC, AM, KM><<<grid5(g, strip), 128, 0, st>>>(g, op, p, z, strip,
+                                                                               ra)));
+}
+
+void launch_op5_apply(const OpDesc& d, const Geom& g, const double* x, double* y,
+                      cudaStream_t st) {
+  const Op5 op = make_op(d);
+  const int strip = d.strip;
+  CHB_DISPATCH(d.kind, (k_op5_apply<BC, AM, KM><<<grid5(g, strip), 128, 0, st>>>(g, op, x, y,
+                                                                                   strip)));
+}
+
+static dim3 grid_pw(const Geom& g) {
+  int gy = g.nyl < 4096 ? g.nyl : 4096;
+  return dim3((g.nx + 255) / 256, gy);
+}
+
+void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace,
+                       const RedArgs& ra, cudaStream_t st) {
+  k_cg5_finish<<<grid_pw(g), 256, 0, st>>>(g, x, p, nullspace, ra);
+}
+
+void launch_sub_mean(const Geom& g, double* x, const KScal* sc, cudaStream_t st) {
+  k_sub_mean<<<grid_pw(g), 256, 0, st>>>(g, x, sc);
+}
+
+void launch_finalize_slabs(const double* tot, int nslabs, int K, const RedArgs& ra,
+                           cudaStream_t st) {
+  k_finalize_slabs<<<1, 32, 0, st>>>(tot, nslabs, K, ra);
+}
+
+}  // namespace chb

@@ -1,0 +1,335 @@
+// kernels_ch.cu -- the 13-point modified Cahn-Hilliard operator
+//   y = x^/dt + (Gamma1/2) L_{M*} Delta_h x^,   x^ = D^{-1} x (right Jacobi)
+// (Eq. 16 4th line with §4's Crank-Nicolson, R5) and
+// the BiCGStab vector updates that run around it (PAPER.md:233-244 names
+// GMRES + Jacobi; BiCGStab is the north_star's GPU choice, R14).
+//
+// The apply stages x^ (halo 2) and phi* (halo 1) in shared memory, forms
+// w = Delta_h x^ on the halo-1 tile in shared memory, then the face-mobility
+// divergence -- one HBM read of x, dinv and phi* per cell, one write of y --
+// and fuses up to two dot products into the same pass.
+#include "common.cuh"
+#include "launch.h"
+
+namespace chb {
+
+constexpr int CTX = 32, CTY = 8;
+
+__device__ __forceinline__ int modc(int c, int nx) {
+  c %= nx;
+  return c < 0 ? c + nx : c;
+}
+
+// Mirror-fold a global row and clamp to the stored range of the slab.
+__device__ __forceinline__ int fold_row(const Geom& g, int gj) {
+  if (gj < 0) gj = -1 - gj;
+  else if (gj >= g.ny) gj = 2 * g.ny - 1 - gj;
+  int lo = g.j0 - GH, hi = g.j0 + g.nyl + GH - 1;
+  if (gj < lo) gj = lo;
+  if (gj > hi) gj = hi;
+  return gj;
+}
+
+template <int NDOT>
+__global__ void __launch_bounds__(CTX* CTY)
+    k_ch_apply(Geom g, ChCoef cc, const double* __restrict__ x, double* __restrict__ y,
+               const double* __restrict__ d1, const double* __restrict__ d2, int skip_done,
+               int skip_half, RedArgs ra) {
+  if (skip_done && ra.sc->done) return;
+  if (skip_half && ra.sc->half) return;
+  __shared__ double xs[CTY + 4][CTX + 4];
+  __shared__ double ps[CTY + 2][CTX + 2];
+  __shared__ double ws[CTY + 2][CTX + 2];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * CTX + tx;
+  const int cx0 = blockIdx.x * CTX;
+  const int jl0 = blockIdx.y * CTY;
+  const int gj0 = g.j0 + jl0;
+  for (int idx = tid; idx < (CTY + 4) * (CTX + 4); idx += CTX * CTY) {
+    const int r = idx / (CTX + 4), c = idx % (CTX + 4);
+    const int gj = fold_row(g, gj0 + r - 2);
+    const int col = modc(cx0 + c - 2, g.nx);
+    const size_t o = off(g, gj, col);
+    double v = x[o];
+    if (cc.dinv) v *= cc.dinv[o];
+    xs[r][c] = v;
+  }
+  for (int idx = tid; idx < (CTY + 2) * (CTX + 2); idx += CTX * CTY) {
+    const int r = idx / (CTX + 2), c = idx % (CTX + 2);
+    const int gj = fold_row(g, gj0 + r - 1);
+    const int col = modc(cx0 + c - 1, g.nx);
+    ps[r][c] = cc.phis[off(g, gj, col)];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < (CTY + 2) * (CTX + 2); idx += CTX * CTY) {
+    const int r = idx / (CTX + 2) + 1, c = idx % (CTX + 2) + 1;
+    ws[r - 1][c - 1] = (xs[r][c + 1] - 2.0 * xs[r][c] + xs[r][c - 1]) * g.ihx2 +
+                       (xs[r + 1][c] - 2.0 * xs[r][c] + xs[r - 1][c]) * g.ihy2;
+  }
+  __syncthreads();
+  const int gj = gj0 + ty, col = cx0 + tx;
+  double s0 = 0.0, s1 = 0.0;
+  if (jl0 + ty < g.nyl && col < g.nx) {
+    const double wc = ws[ty + 1][tx + 1];
+    const double pc = ps[ty + 1][tx + 1];
+    const double L = cc.Lambda;
+    const double mE = L * fmax(0.0, 0.5 * (pc + ps[ty + 1][tx + 2]));
+    const double mW = L * fmax(0.0, 0.5 * (pc + ps[ty + 1][tx]));
+    const double mN = (gj == g.ny - 1) ? 0.0 : L * fmax(0.0, 0.5 * (pc + ps[ty + 2][tx + 1]));
+    const double mS = (gj == 0) ? 0.0 : L * fmax(0.0, 0.5 * (pc + ps[ty][tx + 1]));
+    const double div = (mE * (ws[ty + 1][tx + 2] - wc) - mW * (wc - ws[ty + 1][tx])) * g.ihx2 +
+                       (mN * (ws[ty + 2][tx + 1] - wc) - mS * (wc - ws[ty][tx + 1])) * g.ihy2;
+    const double yv = xs[ty + 2][tx + 2] / cc.dt + cc.g1h * div;
+    const size_t o = off(g, gj, col);
+    y[o] = yv;
+    if (NDOT >= 1) s0 = yv * d1[o];
+    if (NDOT >= 2) s1 = yv * (d2 ? d2[o] : yv);
+  }
+  if (NDOT == 1) {
+    double v[1] = {s0};
+    block_reduce_finalize<1>(v, ra);
+  } else if (NDOT == 2) {
+    double v[2] = {s0, s1};
+    block_reduce_finalize<2>(v, ra);
+  }
+}
+
+void launch_ch_apply(const Geom& g, const ChCoef& cc, const double* x, double* y, int ndot,
+                     const double* d1, const double* d2, int skip_if_done, int skip_if_half,
+                     const RedArgs& ra, cudaStream_t st) {
+  dim3 grid((g.nx + CTX - 1) / CTX, (g.nyl + CTY - 1) / CTY);
+  dim3 block(CTX, CTY);
+  if (ndot == 0)
+    k_ch_apply<0><<<grid, block, 0, st>>>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra);
+  else if (ndot == 1)
+    k_ch_apply<1><<<grid, block, 0, st>>>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra);
+  else
+    k_ch_apply<2><<<grid, block, 0, st>>>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra);
+}
+
+// ------------------------------------------------------- BiCGStab updates
+// Row-parallel pointwise kernels over the slab's own cells.
+#define CHB_PW_LOOP(g)                                              \
+  const int c_ = blockIdx.x * blockDim.x + threadIdx.x;             \
+  for (int jl = blockIdx.y; jl < (g).nyl; jl += gridDim.y)          \
+    if (c_ < (g).nx)
+
+static dim3 grid_pw(const Geom& g) {
+  int gy = g.nyl < 2048 ? g.nyl : 2048;
+  return dim3((g.nx + 255) / 256, gy);
+}
+
+__global__ void __launch_bounds__(256) k_bi_init(Geom g, const double* __restrict__ y,
+                                                 const double* __restrict__ b,
+                                                 double* __restrict__ r, double* __restrict__ rh,
+                                                 RedArgs ra) {
+  double s0 = 0.0, s1 = 0.0;
+  CHB_PW_LOOP(g) {
+    const size_t o = off(g, g.j0 + jl, c_);
+    const double bb = b[o], rr = bb - y[o];
+    r[o] = rr;
+    rh[o] = rr;
+    s0 += bb * bb;
+    s1 += rr * rr;
+  }
+  double v[2] = {s0, s1};
+  block_reduce_finalize<2>(v, ra);
+}
+
+__global__ void __launch_bounds__(256) k_bi_p(Geom g, const double* __restrict__ r,
+                                              double* __restrict__ p, const double* __restrict__ v,
+                                              int first, const KScal* sc) {
+  if (sc->done) return;
+  const double beta = (sc->rho / sc->rho_prev) * (sc->alpha / sc->omega);
+  const double om = sc->omega;
+  CHB_PW_LOOP(g) {
+    const size_t o = off(g, g.j0 + jl, c_);
+    p[o] = first ? r[o] : r[o] + beta * (p[o] - om * v[o]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bi_s(Geom g, const double* __restrict__ r,
+                                              const double* __restrict__ v, double* __restrict__ s,
+                                              RedArgs ra) {
+  if (ra.sc->done) return;
+  const double al = ra.sc->alpha;
+  double acc = 0.0;
+  CHB_PW_LOOP(g) {
+    const size_t o = off(g, g.j0 + jl, c_);
+    const double ss = r[o] - al * v[o];
+    s[o] = ss;
+    acc += ss * ss;
+  }
+  double vv[1] = {acc};
+  block_reduce_finalize<1>(vv, ra);
+}
+
+__global__ void __launch_bounds__(256) k_bi_xr(Geom g, double* __restrict__ x,
+                                               const double* __restrict__ p,
+                                               const double* __restrict__ s,
+                                               const double* __restrict__ t,
+                                               double* __restrict__ r,
+                                               const double* __restrict__ rh,
+                                               const double* __restrict__ dinv, RedArgs ra) {
+  if (ra.sc->done) return;
+  const double al = ra.sc->alpha, om = ra.sc->omega;
+  const int half = ra.sc->half;
+  double a0 = 0.0, a1 = 0.0;
+  CHB_PW_LOOP(g) {
+    const size_t o = off(g, g.j0 + jl, c_);
+    const double di = dinv[o];
+    if (half) {
+      x[o] += al * (di * p[o]);
+    } else {
+      const double ss = s[o];
+      x[o] += al * (di * p[o]) + om * (di * ss);
+      const double rr = ss - om * t[o];
+      r[o] = rr;
+      a0 += rr * rr;
+      a1 += rh[o] * rr;
+    }
+  }
+  double vv[2] = {a0, a1};
+  block_reduce_finalize<2>(vv, ra);
+}
+
+void launch_bi_init(const Geom& g, const double* y, const double* b, double* r, double* rhat,
+                    const RedArgs& ra, cudaStream_t st) {
+  k_bi_init<<<grid_pw(g), 256, 0, st>>>(g, y, b, r, rhat, ra);
+}
+void launch_bi_p(const Geom& g, const double* r, double* p, const double* v, int first,
+                 const KScal* sc, cudaStream_t st) {
+  k_bi_p<<<grid_pw(g), 256, 0, st>>>(g, r, p, v, first, sc);
+}
+void launch_bi_s(const Geom& g, const double* r, const double* v, double* s, const RedArgs& ra,
+                 cudaStream_t st) {
+  k_bi_s<<<grid_pw(g), 256, 0, st>>>(g, r, v, s, ra);
+}
+void launch_bi_xr(const Geom& g, double* x, const double* p, const double* s, const double* t,
+                  double* r, const double* rhat, const double* dinv, const RedArgs& ra,
+                  cudaStream_t st) {
+  k_bi_xr<<<grid_pw(g), 256, 0, st>>>(g, x, p, s, t, r, rhat, dinv, ra);
+}
+
+}  // namespace chb
+
+// ----------------------------------------------------------------- GMRES
+namespace chb {
+
+struct VPtrs {
+  double* v[66];
+};
+
+constexpr int GM_STRIDE = 72;  // partial-sum stride per block (k <= 66)
+
+// out[i] = sum_cells V_i * w  (i < k), deterministic: per-block partials in
+// fixed order, the last block (ticket) reduces them in block order.
+__global__ void __launch_bounds__(256) k_gm_dots(Geom g, VPtrs V, int k,
+                                                 const double* __restrict__ w, double* out,
+                                                 double* part, unsigned int* ticket) {
+  __shared__ double sm[8];
+  __shared__ int am_last;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int bid = blockIdx.x + blockIdx.y * gridDim.x, nb = gridDim.x * gridDim.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = 0; i < k; ++i) {
+    double acc = 0.0;
+    if (c < g.nx)
+      for (int jl = blockIdx.y; jl < g.nyl; jl += gridDim.y) {
+        const size_t o = off(g, g.j0 + jl, c);
+        acc += V.v[i][o] * w[o];
+      }
+    acc = warp_sum(acc);
+    if (lane == 0) sm[wid] = acc;
+    __syncthreads();
+    if (wid == 0) {
+      double t = lane < (int)(blockDim.x >> 5) ? sm[lane] : 0.0;
+      t = warp_sum(t);
+      if (lane == 0) part[(size_t)bid * GM_STRIDE + i] = t;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    __threadfence();
+    am_last = (atomicAdd(ticket, 1u) == (unsigned)(nb - 1));
+  }
+  __syncthreads();
+  if (!am_last || wid != 0) return;
+  __threadfence();
+  for (int i = 0; i < k; ++i) {
+    double t = 0.0;
+    for (int b = lane; b < nb; b += 32) t += __ldcg(part + (size_t)b * GM_STRIDE + i);
+    t = warp_sum(t);
+    if (lane == 0) out[i] = t;
+  }
+  if (lane == 0) *ticket = 0u;
+}
+
+__global__ void __launch_bounds__(256) k_gm_scale(Geom g, double* v, const double* coef) {
+  const double s = coef[0];
+  CHB_PW_LOOP(g) { v[off(g, g.j0 + jl, c_)] *= s; }
+}
+
+__global__ void __launch_bounds__(256) k_gm_axpy_multi(Geom g, VPtrs V, int k,
+                                                       const double* __restrict__ coef,
+                                                       double* __restrict__ w) {
+  CHB_PW_LOOP(g) {
+    const size_t o = off(g, g.j0 + jl, c_);
+    double acc = w[o];
+    for (int i = 0; i < k; ++i) acc -= coef[i] * V.v[i][o];
+    w[o] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gm_residual(Geom g, const double* __restrict__ y,
+                                                     const double* __restrict__ b,
+                                                     double* __restrict__ v0) {
+  CHB_PW_LOOP(g) {
+    const size_t o = off(g, g.j0 + jl, c_);
+    v0[o] = b[o] - y[o];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gm_update_x(Geom g, VPtrs V, int k,
+                                                     const double* __restrict__ coef,
+                                                     const double* __restrict__ dinv,
+                                                     double* __restrict__ x) {
+  CHB_PW_LOOP(g) {
+    const size_t o = off(g, g.j0 + jl, c_);
+    double acc = 0.0;
+    for (int i = 0; i < k; ++i) acc += coef[i] * V.v[i][o];
+    x[o] += dinv[o] * acc;
+  }
+}
+
+static VPtrs vptrs(double* const* V, int k) {
+  VPtrs p;
+  for (int i = 0; i < 66; ++i) p.v[i] = i < k ? V[i] : nullptr;
+  return p;
+}
+
+static dim3 grid_gm(const Geom& g) {
+  int gy = g.nyl < 512 ? g.nyl : 512;
+  return dim3((g.nx + 255) / 256, gy);
+}
+
+void launch_gm_dots(const Geom& g, double* const* V, int k, const double* w, double* out,
+                    double* part, unsigned int* ticket, cudaStream_t st) {
+  k_gm_dots<<<grid_gm(g), 256, 0, st>>>(g, vptrs(V, k), k, w, out, part, ticket);
+}
+void launch_gm_scale(const Geom& g, double* v, const double* coef, cudaStream_t st) {
+  k_gm_scale<<<grid_pw(g), 256, 0, st>>>(g, v, coef);
+}
+void launch_gm_axpy_multi(const Geom& g, double* const* V, int k, const double* coef, double* w,
+                          cudaStream_t st) {
+  k_gm_axpy_multi<<<grid_pw(g), 256, 0, st>>>(g, vptrs(V, k), k, coef, w);
+}
+void launch_gm_residual(const Geom& g, const double* y, const double* b, double* v0,
+                        cudaStream_t st) {
+  k_gm_residual<<<grid_pw(g), 256, 0, st>>>(g, y, b, v0);
+}
+void launch_gm_update_x(const Geom& g, double* const* V, int k, const double* coef,
+                        const double* dinv, double* x, cudaStream_t st) {
+  k_gm_update_x<<<grid_pw(g), 256, 0, st>>>(g, vptrs(V, k), k, coef, dinv, x);
+}
+
+}  // namespace chb

@@ -1,0 +1,114 @@
+// launch.h -- host-side launchers of the device kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace chb {
+
+enum OpKind : int {
+  OPK_POISSON_CONST = 0,
+  OPK_POISSON_VAR = 1,
+  OPK_NUTRIENT = 2,
+  OPK_MOM_U = 3,
+  OPK_MOM_V = 4
+};
+
+// Operator descriptor for the 5-point family (see kernels_cg5.cu).
+struct OpDesc {
+  int kind;
+  int strip;          // rows per marching strip
+  const double* a;    // diagonal coefficient array (NUTRIENT, MOM_*)
+  const double* w;    // cell coefficient (NUTRIENT: phi_s^{1/2}; POISSON_VAR: phi^{n+1})
+  double s, kscale, rho_n, rho_s;
+};
+
+// Algorithmic bytes per cell of the fused CG kernels.
+inline double cg5_bytes_A(int kind) {
+  switch (kind) {
+    case OPK_POISSON_CONST: return 40.0;
+    case OPK_POISSON_VAR: return 48.0;
+    case OPK_NUTRIENT: return 56.0;
+    default: return 48.0;
+  }
+}
+inline double cg5_bytes_B(int kind) {
+  switch (kind) {
+    case OPK_POISSON_CONST: return 24.0;
+    case OPK_POISSON_VAR: return 32.0;
+    case OPK_NUTRIENT: return 40.0;
+    default: return 32.0;
+  }
+}
+
+void launch_cg5_init(const OpDesc& d, const Geom& g, const double* x, const double* b,
+                     int use_shift, double* z, const RedArgs& ra, cudaStream_t st);
+void launch_cg5_A(const OpDesc& d, const Geom& g, const double* z, const double* po, double* pn,
+                  double* x, int first, const RedArgs& ra, cudaStream_t st);
+void launch_cg5_B(const OpDesc& d, const Geom& g, const double* p, double* z, const RedArgs& ra,
+                  cudaStream_t st);
+void launch_op5_apply(const OpDesc& d, const Geom& g, const double* x, double* y,
+                      cudaStream_t st);
+void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace,
+                       const RedArgs& ra, cudaStream_t st);
+void launch_sub_mean(const Geom& g, double* x, const KScal* sc, cudaStream_t st);
+void launch_finalize_slabs(const double* tot, int nslabs, int K, const RedArgs& ra,
+                           cudaStream_t st);
+
+// ---- Cahn-Hilliard 13-point operator and BiCGStab / GMRES vector kernels
+struct ChCoef {
+  const double* phis;  // phi* (mobility source)
+  const double* dinv;  // Jacobi inverse diagonal (nullptr: no scaling)
+  double dt, g1h, Lambda;  // g1h = Gamma1 / 2
+};
+// y = A (dinv .* x)  [or A x when dinv == nullptr]; fused dots:
+//   ndot = 0: none; 1: (y, d1); 2: (y, d1), (y, d2) where d2 == nullptr means (y, y)
+void launch_ch_apply(const Geom& g, const ChCoef& cc, const double* x, double* y, int ndot,
+                     const double* d1, const double* d2, int skip_if_done, int skip_if_half,
+                     const RedArgs& ra, cudaStream_t st);
+
+void launch_bi_init(const Geom& g, const double* y, const double* b, double* r, double* rhat,
+                    const RedArgs& ra, cudaStream_t st);
+void launch_bi_p(const Geom& g, const double* r, double* p, const double* v, int first,
+                 const KScal* sc, cudaStream_t st);
+void launch_bi_s(const Geom& g, const double* r, const double* v, double* s, const RedArgs& ra,
+                 cudaStream_t st);
+void launch_bi_xr(const Geom& g, double* x, const double* p, const double* s, const double* t,
+                  double* r, const double* rhat, const double* dinv, const RedArgs& ra,
+                  cudaStream_t st);
+
+// GMRES (classical Gram-Schmidt with one re-orthogonalisation, CGS2); V has <= 66 vectors
+void launch_gm_dots(const Geom& g, double* const* V, int k, const double* w, double* out,
+                    double* part, unsigned int* ticket, cudaStream_t st);
+void launch_gm_scale(const Geom& g, double* v, const double* coef, cudaStream_t st);
+void launch_gm_axpy_multi(const Geom& g, double* const* V, int k, const double* coef, double* w,
+                          cudaStream_t st);
+void launch_gm_residual(const Geom& g, const double* y, const double* b, double* v0,
+                        cudaStream_t st);
+void launch_gm_update_x(const Geom& g, double* const* V, int k, const double* coef,
+                        const double* dinv, double* x, cudaStream_t st);
+
+// ---- explicit right-hand sides and projection (kernels_rhs.cu)
+struct Phys {
+  double dt, Gamma1, Gamma2, Lambda, mu, Kc, eps, A, Ds, Re_s, Re_n, rho_n, rho_s, lid_u;
+};
+struct StateP {
+  const double *phi, *phip, *c, *u, *v, *p;
+};
+void launch_ch_rhs(const Geom& g, const Phys& ph, StateP s, double* phis, double* dinv,
+                   double* b, cudaStream_t st);
+void launch_nut_rhs(const Geom& g, const Phys& ph, StateP s, const double* phi1, double* a,
+                    double* w, double* b, cudaStream_t st);
+void launch_mom_rhs_u(const Geom& g, const Phys& ph, StateP s, const double* phis, double* a,
+                      double* b, cudaStream_t st);
+void launch_mom_rhs_v(const Geom& g, const Phys& ph, StateP s, const double* phis, double* a,
+                      double* b, cudaStream_t st);
+void launch_mom_coef(const Geom& g, const Phys& ph, const double* phis, double* au, double* av,
+                     cudaStream_t st);
+void launch_div(const Geom& g, const double* us, const double* vs, double* b, const RedArgs& ra,
+                cudaStream_t st);
+void launch_project(const Geom& g, const Phys& ph, const double* phi1, const double* us,
+                    const double* vs, const double* p, double* u, double* v, cudaStream_t st);
+void launch_copy_rows(const Geom& g, const double* src, double* dst, cudaStream_t st);
+
+}  // namespace chb

@@ -1,0 +1,172 @@
+"""GPU path (C ABI, sm_100a kernels) vs the CPU oracle, element by element.
+
+Tolerances (north_star): relative L2 <= 1e-9 per field after one step,
+<= 1e-6 after 100 steps; every Krylov solve reaches ||r||/||b|| <= 1e-10.
+Operator applies are exact up to rounding: relative L2 <= 1e-13.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("phi", "c", "u", "v", "p")
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+def _oracle_params(sp, **kw):
+    from oracle import Params
+    d = dict(dt=sp.dt, Gamma1=sp.Gamma1, Gamma2=sp.Gamma2, Lambda=sp.Lambda, mu=sp.mu, Kc=sp.Kc,
+             eps=sp.eps, A=sp.A, Ds=sp.Ds, Re_s=sp.Re_s, Re_n=sp.Re_n, rho_n=sp.rho_n,
+             rho_s=sp.rho_s, lid_u=sp.lid_u, rtol=sp.rtol, maxit=sp.maxit,
+             ch_solver=sp.ch_solver, gmres_restart=sp.gmres_restart)
+    d.update(kw)
+    return Params(**d)
+
+
+def _run_both(nx, ny, steps, seed=0, slabs=1, **over):
+    from paper_1811_11842_b200 import Simulation, SimParams
+    from oracle import initial_state, step
+    from workloads import initial_fields
+    f = initial_fields(nx, ny, seed=seed)
+    sp = SimParams(**over)
+    sim = Simulation(nx, ny, sp, virtual_slabs=slabs)
+    sim.set_fields(**f)
+    sim.step(steps)
+    got = sim.get_fields()
+    st = sim.stats()
+    sim.close()
+    ost = initial_state(f)
+    prm = _oracle_params(sp)
+    iters = []
+    for _ in range(steps):
+        ost, info = step(ost, prm)
+        iters.append(info.iters)
+    ref = dict(phi=ost.phi, c=ost.c, u=ost.u, v=ost.v, p=ost.p)
+    return got, ref, st, iters
+
+
+@pytest.mark.parametrize("nx,ny", [(64, 64), (50, 37), (130, 70)])
+def test_one_step_matches_oracle(nx, ny):
+    got, ref, st, iters = _run_both(nx, ny, 1)
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
+    for sysname, n in iters[-1].items():
+        assert abs(st["iters_last"][sysname] - n) <= 2, (sysname, st["iters_last"], iters[-1])
+        assert st["resid_last"][sysname] <= 1e-10
+
+
+def test_one_step_gmres_matches_oracle():
+    got, ref, st, _ = _run_both(64, 64, 1, ch_solver="gmres", Lambda=1e-3)
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
+
+
+def test_bicgstab_nontrivial_ch_system():
+    """Lambda large enough that the CH system is far from I/dt (many iterations)."""
+    got, ref, st, iters = _run_both(48, 40, 2, Lambda=1e-3)
+    assert st["iters_last"]["ch"] >= 5
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
+
+
+@pytest.mark.parametrize("slabs", [2, 3])
+def test_virtual_slabs_match_single_slab(slabs):
+    """Slab decomposition in y with halo exchange reproduces the 1-slab step."""
+    from paper_1811_11842_b200 import Simulation
+    from workloads import initial_fields
+    f = initial_fields(40, 36, seed=4)
+    out = []
+    for s in (1, slabs):
+        sim = Simulation(40, 36, virtual_slabs=s, Lambda=1e-3)
+        sim.set_fields(**f)
+        sim.step(2)
+        out.append(sim.get_fields())
+        sim.close()
+    for k in FIELDS:
+        assert _rel(out[1][k], out[0][k]) <= 1e-12, (k, _rel(out[1][k], out[0][k]))
+
+
+def test_operator_applies_match_assembled_matrices():
+    from paper_1811_11842_b200 import Simulation
+    from oracle import assemble as asm, explicit as ex
+    from oracle.step import initial_state, momentum_systems
+    from oracle.params import Params
+    from workloads import initial_fields
+    nx, ny = 45, 38
+    f = initial_fields(nx, ny, seed=1)
+    rng = np.random.default_rng(0)
+    x = rng.random((ny, nx))
+    prm = Params(Lambda=1e-3)
+    sim = Simulation(nx, ny, Lambda=1e-3)
+    sim.set_fields(**f)
+    st = initial_state(f)
+    phs = ex.phi_star(st.phi, st.phi_prev)
+    Mx, My = ex.mobility_faces(phs, prm.Lambda)
+    A = asm.ch_matrix(nx, ny, prm.dt, prm.Gamma1, Mx, My)
+    assert _rel(sim.apply_operator("ch", x).ravel(), A @ x.ravel()) <= 1e-13
+    bx, by = ex.pressure_faces(st.phi, prm.rho_n, prm.rho_s)
+    Ap = asm.poisson_matrix(nx, ny, bx, by)
+    assert _rel(sim.apply_operator("poisson", x).ravel(), Ap @ x.ravel()) <= 1e-13
+    (Au, _), (Av, _) = momentum_systems(st, phs, prm)
+    assert _rel(sim.apply_operator("mom_u", x).ravel(), Au @ x.ravel()) <= 1e-13
+    xv = x.copy()
+    xv[0] = 0.0
+    assert _rel(sim.apply_operator("mom_v", xv).ravel(), Av @ xv.ravel()) <= 1e-13
+    sim.close()
+
+
+def test_variable_density_poisson_operator():
+    from paper_1811_11842_b200 import Simulation
+    from oracle import assemble as asm, explicit as ex
+    from workloads import initial_fields
+    nx, ny = 33, 29
+    f = initial_fields(nx, ny, seed=3)
+    x = np.random.default_rng(5).random((ny, nx))
+    sim = Simulation(nx, ny, rho_n=1.7, rho_s=0.9)
+    sim.set_fields(**f)
+    bx, by = ex.pressure_faces(f["phi"], 1.7, 0.9)
+    Ap = asm.poisson_matrix(nx, ny, bx, by)
+    assert _rel(sim.apply_operator("poisson", x).ravel(), Ap @ x.ravel()) <= 1e-13
+    sim.close()
+
+
+def test_variable_density_step_matches_oracle():
+    got, ref, _, _ = _run_both(40, 32, 1, rho_n=1.5, rho_s=1.0)
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
+
+
+def test_device_buffers_roundtrip():
+    import torch
+    from paper_1811_11842_b200 import Simulation
+    from workloads import initial_fields
+    f = initial_fields(32, 32, seed=2)
+    sim = Simulation(32, 32)
+    dev = {k: torch.from_numpy(v).cuda() for k, v in f.items()}
+    sim.set_fields(**dev)
+    back = sim.get_fields(device=True)
+    torch.cuda.synchronize()
+    for k in FIELDS:
+        assert np.array_equal(back[k].cpu().numpy(), f[k])
+    sim.close()
+
+
+def test_mass_conserved_and_divergence_free_on_gpu():
+    from paper_1811_11842_b200 import Simulation
+    from oracle import explicit as ex
+    from workloads import initial_fields
+    f = initial_fields(96, 96, seed=8)
+    sim = Simulation(96, 96, eps=0.0)
+    sim.set_fields(**f)
+    m0 = ex.mass(f["phi"])
+    for _ in range(5):
+        sim.step(1)
+        g = sim.get_fields()
+        assert abs(ex.mass(g["phi"]) - m0) / m0 < 1e-12
+        d = ex.divergence(g["u"], g["v"])
+        assert np.abs(d).max() < 1e-6
+    sim.close()
