@@ -3,6 +3,7 @@
 // time-step orchestration of DESIGN.md §1.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -74,6 +75,8 @@ struct ch_handle {
   size_t arr_elems = 0;
   double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
   double* gm_host = nullptr;  // pinned mirror
+  int vec = 1;                // vectorised CG kernels (env CHB_VEC=0 disables)
+  int strip2 = 32;            // rows per strip (env CHB_STRIP)
 };
 
 namespace {
@@ -283,6 +286,8 @@ OpDesc opdesc(ch_handle* h, int kind, const Slab& s) {
   OpDesc d;
   d.kind = kind;
   d.strip = 16;
+  d.strip2 = h->strip2;
+  d.vec = h->vec;
   d.a = nullptr;
   d.w = nullptr;
   d.s = 1.0;
@@ -823,6 +828,8 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   h->prm = *params;
   h->S = S;
   h->nslabs_total = total;
+  if (const char* e = getenv("CHB_VEC")) h->vec = atoi(e);
+  if (const char* e = getenv("CHB_STRIP")) h->strip2 = std::max(1, atoi(e));
   memset(&h->stats, 0, sizeof(ch_stats));
   // rows: balanced split of ny over `total` slabs (first ny % total get one more)
   const int base = G.ny / total, rem = G.ny % total;

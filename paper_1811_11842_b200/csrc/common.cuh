@@ -115,7 +115,7 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
       break;
     }
     case FIN_CG_A: {
-      if (!(t[0] > 0.0) || !(s->rho == s->rho)) { s->status = 1; s->done = 1; break; }
+      if (bad(t[0]) || !(s->rho == s->rho)) { s->status = 1; s->done = 1; break; }
       s->alpha = s->rho / t[0];
       break;
     }

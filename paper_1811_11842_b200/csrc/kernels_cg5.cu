@@ -283,6 +283,227 @@ __global__ void __launch_bounds__(128) k_op5_apply(Geom g, Op5 op, const double*
   }
 }
 
+// ===================================================================== v2
+// Vectorised marching kernels (even nx): each thread owns two adjacent
+// columns (16-B loads/stores), rows are prefetched two ahead so every warp
+// keeps two rows of loads in flight, and the strip index can be traversed in
+// reverse (B after A reverses, so B starts on the rows A touched last and
+// finds them in L2).
+template <int BC>
+__device__ __forceinline__ double2 ld2(const double* __restrict__ a, const Geom& g, int gj, int c) {
+  if (BC == BC_VFACE) {
+    if (gj <= 0 || gj >= g.ny) return make_double2(0.0, 0.0);
+    return *reinterpret_cast<const double2*>(a + off(g, gj, c));
+  }
+  double s = 1.0;
+  if (gj < 0) {
+    gj = -1 - gj;
+    s = (BC == BC_ODD) ? -1.0 : 1.0;
+  } else if (gj >= g.ny) {
+    gj = 2 * g.ny - 1 - gj;
+    s = (BC == BC_ODD) ? -1.0 : 1.0;
+  }
+  double2 v = *reinterpret_cast<const double2*>(a + off(g, gj, c));
+  v.x *= s;
+  v.y *= s;
+  return v;
+}
+
+struct Col2 {
+  int c0, cc, cw, ce, lane;
+  bool act, needW, needE;
+  __device__ __forceinline__ Col2(const Geom& g) {
+    lane = threadIdx.x & 31;
+    c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    act = c0 < g.nx;
+    cc = act ? c0 : g.nx - 2;
+    cw = wrapc(cc - 1, g.nx);
+    ce = wrapc(cc + 2, g.nx);
+    needW = (lane == 0) || (c0 == 0);
+    needE = (lane == 31) || (c0 + 2 >= g.nx);
+  }
+};
+
+// One row of an unknown-type stream: own two columns + the two outer neighbours.
+struct R2 {
+  double2 v;
+  double w, e;
+};
+
+template <int BC>
+__device__ __forceinline__ R2 ldrow(const double* __restrict__ a, const Geom& g, const Col2& col,
+                                    int gj) {
+  R2 r;
+  r.v = ld2<BC>(a, g, gj, col.cc);
+  r.w = col.needW ? ldf<BC>(a, g, gj, col.cw) : 0.0;
+  r.e = col.needE ? ldf<BC>(a, g, gj, col.ce) : 0.0;
+  return r;
+}
+
+// fill the outer neighbours from the adjacent lanes where they live there
+__device__ __forceinline__ void xnb(const Col2& col, double2 v, double& w, double& e) {
+  const double sw = __shfl_up_sync(FULL, v.y, 1);
+  const double se = __shfl_down_sync(FULL, v.x, 1);
+  if (!col.needW) w = sw;
+  if (!col.needE) e = se;
+}
+
+template <int BC, int AM, int KM>
+__device__ __forceinline__ void eval_pair(const Op5& op, const Geom& g, int gj, double2 ac,
+                                          double2 wc, double ww, double we, double2 ws, double2 wn,
+                                          double2 xc, double xw, double xe, double2 xs, double2 xn,
+                                          double2& y, double2& d) {
+  eval5<BC, AM, KM>(op, g, gj, ac.x, wc.x, ww, wc.y, ws.x, wn.x, xc.x, xw, xc.y, xs.x, xn.x, y.x,
+                    d.x);
+  eval5<BC, AM, KM>(op, g, gj, ac.y, wc.y, wc.x, we, ws.y, wn.y, xc.y, xc.x, xe, xs.y, xn.y, y.y,
+                    d.y);
+}
+
+// A: p = z + beta p_old; x += alpha p_old; q = A p; reduce (p, q)
+template <int BC, int AM, int KM>
+__global__ void __launch_bounds__(128) k_cg5_A2(Geom g, Op5 op, const double* __restrict__ z,
+                                                const double* __restrict__ po,
+                                                double* __restrict__ pn, double* __restrict__ x,
+                                                int first, int strip, int reverse, RedArgs ra) {
+  if (ra.sc->done) return;
+  const double beta = first ? 0.0 : ra.sc->beta;
+  const double alpha = first ? 0.0 : ra.sc->alpha;
+  const Col2 col(g);
+  const int by = reverse ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y;
+  const int jl0 = by * strip, jl1 = min(jl0 + strip, g.nyl);
+  int gj = g.j0 + jl0;
+  auto comb = [&](const R2& zr, const R2& pr) {
+    R2 o;
+    o.v.x = zr.v.x + beta * pr.v.x;
+    o.v.y = zr.v.y + beta * pr.v.y;
+    o.w = zr.w + beta * pr.w;
+    o.e = zr.e + beta * pr.e;
+    return o;
+  };
+  auto P = [&](int r) {
+    R2 zr = ldrow<BC>(z, g, col, r);
+    if (first) return zr;
+    return comb(zr, ldrow<BC>(po, g, col, r));
+  };
+  R2 Pm = P(gj - 1), P0 = P(gj);
+  R2 z1 = ldrow<BC>(z, g, col, gj + 1);
+  R2 p1 = first ? z1 : ldrow<BC>(po, g, col, gj + 1);
+  R2 Wm, W0, W1;
+  if (KM) {
+    Wm = ldrow<BC_MIRROR>(op.w, g, col, gj - 1);
+    W0 = ldrow<BC_MIRROR>(op.w, g, col, gj);
+    W1 = ldrow<BC_MIRROR>(op.w, g, col, gj + 1);
+  }
+  double acc = 0.0;
+  for (int jl = jl0; jl < jl1; ++jl, ++gj) {
+    // prefetch row gj + 2
+    R2 z2, p2, W2;
+    if (jl + 1 < jl1) {
+      z2 = ldrow<BC>(z, g, col, gj + 2);
+      if (!first) p2 = ldrow<BC>(po, g, col, gj + 2);
+      if (KM) W2 = ldrow<BC_MIRROR>(op.w, g, col, gj + 2);
+    }
+    double2 ac = make_double2(0.0, 0.0), xo = make_double2(0.0, 0.0), poc = make_double2(0.0, 0.0);
+    const size_t o = off(g, gj, col.cc);
+    if (AM) ac = *reinterpret_cast<const double2*>(op.a + o);
+    if (!first) {
+      xo = *reinterpret_cast<const double2*>(x + o);
+      poc = *reinterpret_cast<const double2*>(po + o);
+    }
+    const R2 Pp = first ? z1 : comb(z1, p1);
+    double pw = P0.w, pe = P0.e;
+    xnb(col, P0.v, pw, pe);
+    double ww = 0.0, we = 0.0;
+    if (KM) {
+      ww = W0.w;
+      we = W0.e;
+      xnb(col, W0.v, ww, we);
+    }
+    double2 y, d;
+    eval_pair<BC, AM, KM>(op, g, gj, ac, W0.v, ww, we, Wm.v, W1.v, P0.v, pw, pe, Pm.v, Pp.v, y, d);
+    if (col.act) {
+      *reinterpret_cast<double2*>(pn + o) = P0.v;
+      if (!first) {
+        xo.x += alpha * poc.x;
+        xo.y += alpha * poc.y;
+        *reinterpret_cast<double2*>(x + o) = xo;
+      }
+      acc += P0.v.x * y.x + P0.v.y * y.y;
+    }
+    Pm = P0;
+    P0 = Pp;
+    z1 = z2;
+    p1 = first ? z2 : p2;
+    if (KM) {
+      Wm = W0;
+      W0 = W1;
+      W1 = W2;
+    }
+  }
+  double v[1] = {acc};
+  block_reduce_finalize<1>(v, ra);
+}
+
+// B: r = d z - alpha A p; z = r / d; reduce (r, z), (r, r)
+template <int BC, int AM, int KM>
+__global__ void __launch_bounds__(128) k_cg5_B2(Geom g, Op5 op, const double* __restrict__ p,
+                                                double* __restrict__ z, int strip, int reverse,
+                                                RedArgs ra) {
+  if (ra.sc->done) return;
+  const double alpha = ra.sc->alpha;
+  const Col2 col(g);
+  const int by = reverse ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y;
+  const int jl0 = by * strip, jl1 = min(jl0 + strip, g.nyl);
+  int gj = g.j0 + jl0;
+  R2 Pm = ldrow<BC>(p, g, col, gj - 1), P0 = ldrow<BC>(p, g, col, gj),
+     P1 = ldrow<BC>(p, g, col, gj + 1);
+  R2 Wm, W0, W1;
+  if (KM) {
+    Wm = ldrow<BC_MIRROR>(op.w, g, col, gj - 1);
+    W0 = ldrow<BC_MIRROR>(op.w, g, col, gj);
+    W1 = ldrow<BC_MIRROR>(op.w, g, col, gj + 1);
+  }
+  double s0 = 0.0, s1 = 0.0;
+  for (int jl = jl0; jl < jl1; ++jl, ++gj) {
+    R2 P2, W2;
+    if (jl + 1 < jl1) {
+      P2 = ldrow<BC>(p, g, col, gj + 2);
+      if (KM) W2 = ldrow<BC_MIRROR>(op.w, g, col, gj + 2);
+    }
+    const size_t o = off(g, gj, col.cc);
+    double2 ac = make_double2(0.0, 0.0);
+    if (AM) ac = *reinterpret_cast<const double2*>(op.a + o);
+    const double2 zc = *reinterpret_cast<const double2*>(z + o);
+    double pw = P0.w, pe = P0.e;
+    xnb(col, P0.v, pw, pe);
+    double ww = 0.0, we = 0.0;
+    if (KM) {
+      ww = W0.w;
+      we = W0.e;
+      xnb(col, W0.v, ww, we);
+    }
+    double2 y, d;
+    eval_pair<BC, AM, KM>(op, g, gj, ac, W0.v, ww, we, Wm.v, W1.v, P0.v, pw, pe, Pm.v, P1.v, y, d);
+    if (col.act) {
+      const double rx = d.x * zc.x - alpha * y.x, ry = d.y * zc.y - alpha * y.y;
+      const double2 zn = make_double2(rx / d.x, ry / d.y);
+      *reinterpret_cast<double2*>(z + o) = zn;
+      s0 += rx * zn.x + ry * zn.y;
+      s1 += rx * rx + ry * ry;
+    }
+    Pm = P0;
+    P0 = P1;
+    P1 = P2;
+    if (KM) {
+      Wm = W0;
+      W0 = W1;
+      W1 = W2;
+    }
+  }
+  double v[2] = {s0, s1};
+  block_reduce_finalize<2>(v, ra);
+}
+
 // ---------------------------------------------------------------- CG finish
 // x += alpha p (last iteration's update, deferred by the A kernel), or x = 0
 // when b = 0; optional reduction of sum(x) for the null-space projection.
@@ -362,9 +583,19 @@ void launch_cg5_init(const OpDesc& d, const Geom& g, const double* x, const doub
                            g, op, x, b, use_shift, z, strip, ra)));
 }
 
+static dim3 grid5v(const Geom& g, int strip) {
+  return dim3((g.nx + 255) / 256, (g.nyl + strip - 1) / strip);
+}
+
 void launch_cg5_A(const OpDesc& d, const Geom& g, const double* z, const double* po, double* pn,
                   double* x, int first, const RedArgs& ra, cudaStream_t st) {
   const Op5 op = make_op(d);
+  if (d.vec && (g.nx % 2 == 0)) {
+    const int strip = d.strip2;
+    CHB_DISPATCH(d.kind, (k_cg5_A2<BC, AM, KM><<<grid5v(g, strip), 128, 0, st>>>(
+                             g, op, z, po, pn, x, first, strip, 0, ra)));
+    return;
+  }
   const int strip = d.strip;
   CHB_DISPATCH(d.kind, (k_cg5_A<BC, AM, KM><<<grid5(g, strip), 128, 0, st>>>(
                            g, op, z, po, pn, x, first, strip, ra)));
@@ -373,6 +604,12 @@ void launch_cg5_A(const OpDesc& d, const Geom& g, const double* z, const double*
 void launch_cg5_B(const OpDesc& d, const Geom& g, const double* p, double* z, const RedArgs& ra,
                   cudaStream_t st) {
   const Op5 op = make_op(d);
+  if (d.vec && (g.nx % 2 == 0)) {
+    const int strip = d.strip2;
+    CHB_DISPATCH(d.kind, (k_cg5_B2<BC, AM, KM><<<grid5v(g, strip), 128, 0, st>>>(
+                             g, op, p, z, strip, 1, ra)));
+    return;
+  }
   const int strip = d.strip;
   CHB_DISPATCH(d.kind, (k_cg5_B<BC, AM, KM><<<grid5(g, strip), 128, 0, st>>>(g, op, p, z, strip,
                                                                                ra)));

@@ -17,7 +17,9 @@ enum OpKind : int {
 // Operator descriptor for the 5-point family (see kernels_cg5.cu).
 struct OpDesc {
   int kind;
-  int strip;          // rows per marching strip
+  int strip;          // rows per marching strip (scalar kernels)
+  int strip2;         // rows per strip of the vectorised kernels
+  int vec;            // use the 2-column vectorised kernels when nx is even
   const double* a;    // diagonal coefficient array (NUTRIENT, MOM_*)
   const double* w;    // cell coefficient (NUTRIENT: phi_s^{1/2}; POISSON_VAR: phi^{n+1})
   double s, kscale, rho_n, rho_s;

@@ -60,14 +60,14 @@ def test_one_step_matches_oracle(nx, ny):
 
 
 def test_one_step_gmres_matches_oracle():
-    got, ref, st, _ = _run_both(64, 64, 1, ch_solver="gmres", Lambda=1e-3)
+    got, ref, st, _ = _run_both(64, 64, 1, ch_solver="gmres", Lambda=1e-5)
     for k in FIELDS:
         assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
 
 
 def test_bicgstab_nontrivial_ch_system():
     """Lambda large enough that the CH system is far from I/dt (many iterations)."""
-    got, ref, st, iters = _run_both(48, 40, 2, Lambda=1e-3)
+    got, ref, st, iters = _run_both(48, 40, 2, Lambda=1e-5)
     assert st["iters_last"]["ch"] >= 5
     for k in FIELDS:
         assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
@@ -75,19 +75,58 @@ def test_bicgstab_nontrivial_ch_system():
 
 @pytest.mark.parametrize("slabs", [2, 3])
 def test_virtual_slabs_match_single_slab(slabs):
-    """Slab decomposition in y with halo exchange reproduces the 1-slab step."""
+    """Slab decomposition in y with halo exchange reproduces the 1-slab step.
+    The Krylov dot products sum in a different order per decomposition, so the
+    comparison runs the solves to rtol = 1e-13 (differences are then rounding
+    propagated through ~200 CG iterations, not solver tolerance)."""
     from paper_1811_11842_b200 import Simulation
     from workloads import initial_fields
     f = initial_fields(40, 36, seed=4)
-    out = []
+    out, its = [], []
     for s in (1, slabs):
-        sim = Simulation(40, 36, virtual_slabs=s, Lambda=1e-3)
+        sim = Simulation(40, 36, virtual_slabs=s, Lambda=1e-5, rtol=1e-13)
         sim.set_fields(**f)
         sim.step(2)
         out.append(sim.get_fields())
+        its.append(sim.stats()["iters_last"])
         sim.close()
     for k in FIELDS:
-        assert _rel(out[1][k], out[0][k]) <= 1e-12, (k, _rel(out[1][k], out[0][k]))
+        assert _rel(out[1][k], out[0][k]) <= 1e-11, (k, _rel(out[1][k], out[0][k]))
+    for k in its[0]:
+        assert abs(its[0][k] - its[1][k]) <= 3, its
+
+
+def test_virtual_slabs_gmres():
+    from paper_1811_11842_b200 import Simulation
+    from workloads import initial_fields
+    f = initial_fields(36, 32, seed=6)
+    out = []
+    for s in (1, 2):
+        sim = Simulation(36, 32, virtual_slabs=s, Lambda=1e-5, rtol=1e-13, ch_solver="gmres")
+        sim.set_fields(**f)
+        sim.step(1)
+        out.append(sim.get_fields())
+        sim.close()
+    for k in FIELDS:
+        assert _rel(out[1][k], out[0][k]) <= 1e-11, (k, _rel(out[1][k], out[0][k]))
+
+
+def test_hundred_steps_256_matches_oracle_golden():
+    """BASELINE.json configs[1]: 256^2, 100 steps, dt = 1e-4 vs the oracle's
+    fields (tests/golden/oracle_256_100.npz, written by scripts/gen_golden.py
+    from oracle/ only); north_star tolerance 1e-6 relative L2."""
+    import os
+    from paper_1811_11842_b200 import Simulation
+    from workloads import initial_fields
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "oracle_256_100.npz"))
+    f = initial_fields(256, 256, seed=int(gold["seed"]))
+    sim = Simulation(256, 256)
+    sim.set_fields(**f)
+    sim.step(100)
+    got = sim.get_fields()
+    sim.close()
+    for k in FIELDS:
+        assert _rel(got[k], gold[k]) <= 1e-6, (k, _rel(got[k], gold[k]))
 
 
 def test_operator_applies_match_assembled_matrices():
