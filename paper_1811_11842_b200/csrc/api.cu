@@ -75,8 +75,8 @@ struct ch_handle {
   size_t arr_elems = 0;
   double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
   double* gm_host = nullptr;  // pinned mirror
-  int vec = 1;                // vectorised CG kernels (env CHB_VEC=0 disables)
-  int strip2 = 32;            // rows per strip (env CHB_STRIP)
+  int vec = 2;                // CG kernels: 2 TMA ring, 1 register pipeline, 0 scalar (env CHB_VEC)
+  int strip2 = 0;             // rows per strip, 0 = one resident wave (env CHB_STRIP)
 };
 
 namespace {
@@ -829,7 +829,7 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   h->S = S;
   h->nslabs_total = total;
   if (const char* e = getenv("CHB_VEC")) h->vec = atoi(e);
-  if (const char* e = getenv("CHB_STRIP")) h->strip2 = std::max(1, atoi(e));
+  if (const char* e = getenv("CHB_STRIP")) h->strip2 = std::max(0, atoi(e));
   memset(&h->stats, 0, sizeof(ch_stats));
   // rows: balanced split of ny over `total` slabs (first ny % total get one more)
   const int base = G.ny / total, rem = G.ny % total;

@@ -359,58 +359,64 @@ __device__ __forceinline__ void eval_pair(const Op5& op, const Geom& g, int gj, 
                     d.y);
 }
 
-// A: p = z + beta p_old; x += alpha p_old; q = A p; reduce (p, q)
+// Raw loads of one row for the CG half-iterations.  Rows are consumed one
+// iteration after they are issued (prefetch distance 2), so each warp keeps
+// two rows of loads in flight.
+struct RawA {
+  R2 z, p, w;
+  double2 x, a;
+};
+
 template <int BC, int AM, int KM>
-__global__ void __launch_bounds__(128) k_cg5_A2(Geom g, Op5 op, const double* __restrict__ z,
+__device__ __forceinline__ void load_rawA(RawA& r, const Geom& g, const Col2& col, const Op5& op,
+                                          const double* __restrict__ z,
+                                          const double* __restrict__ po,
+                                          const double* __restrict__ x, int gj, bool first,
+                                          bool centre) {
+  r.z = ldrow<BC>(z, g, col, gj);
+  if (!first) r.p = ldrow<BC>(po, g, col, gj);
+  if (KM) r.w = ldrow<BC_MIRROR>(op.w, g, col, gj);
+  if (centre) {
+    const size_t o = off(g, gj, col.cc);
+    if (!first) r.x = *reinterpret_cast<const double2*>(x + o);
+    if (AM) r.a = *reinterpret_cast<const double2*>(op.a + o);
+  }
+}
+
+// A: p = z + beta p_old; x += alpha p_old; q = A p; reduce (p, q).
+// DIR = +1 marches a strip upward in j, -1 downward (alternated with B).
+template <int BC, int AM, int KM, int DIR>
+__global__ void __launch_bounds__(128) k_cg5_A3(Geom g, Op5 op, const double* __restrict__ z,
                                                 const double* __restrict__ po,
                                                 double* __restrict__ pn, double* __restrict__ x,
-                                                int first, int strip, int reverse, RedArgs ra) {
+                                                int first, int strip, RedArgs ra) {
   if (ra.sc->done) return;
   const double beta = first ? 0.0 : ra.sc->beta;
   const double alpha = first ? 0.0 : ra.sc->alpha;
   const Col2 col(g);
-  const int by = reverse ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y;
-  const int jl0 = by * strip, jl1 = min(jl0 + strip, g.nyl);
-  int gj = g.j0 + jl0;
-  auto comb = [&](const R2& zr, const R2& pr) {
+  const int jl0 = blockIdx.y * strip, jl1 = min(jl0 + strip, g.nyl);
+  const int jb = DIR > 0 ? jl0 : jl1 - 1;       // first row marched
+  const int n = jl1 - jl0;
+  auto comb = [&](const RawA& r) {
+    if (first) return r.z;
     R2 o;
-    o.v.x = zr.v.x + beta * pr.v.x;
-    o.v.y = zr.v.y + beta * pr.v.y;
-    o.w = zr.w + beta * pr.w;
-    o.e = zr.e + beta * pr.e;
+    o.v.x = r.z.v.x + beta * r.p.v.x;
+    o.v.y = r.z.v.y + beta * r.p.v.y;
+    o.w = r.z.w + beta * r.p.w;
+    o.e = r.z.e + beta * r.p.e;
     return o;
   };
-  auto P = [&](int r) {
-    R2 zr = ldrow<BC>(z, g, col, r);
-    if (first) return zr;
-    return comb(zr, ldrow<BC>(po, g, col, r));
-  };
-  R2 Pm = P(gj - 1), P0 = P(gj);
-  R2 z1 = ldrow<BC>(z, g, col, gj + 1);
-  R2 p1 = first ? z1 : ldrow<BC>(po, g, col, gj + 1);
-  R2 Wm, W0, W1;
-  if (KM) {
-    Wm = ldrow<BC_MIRROR>(op.w, g, col, gj - 1);
-    W0 = ldrow<BC_MIRROR>(op.w, g, col, gj);
-    W1 = ldrow<BC_MIRROR>(op.w, g, col, gj + 1);
-  }
+  RawA rb, r0, r1, r2;
+  int gj = g.j0 + jb;
+  load_rawA<BC, AM, KM>(rb, g, col, op, z, po, x, gj - DIR, first, false);
+  load_rawA<BC, AM, KM>(r0, g, col, op, z, po, x, gj, first, true);
+  load_rawA<BC, AM, KM>(r1, g, col, op, z, po, x, gj + DIR, first, n > 1);
+  R2 Pb = comb(rb), P0 = comb(r0);
+  R2 Wb = rb.w, W0 = r0.w;
   double acc = 0.0;
-  for (int jl = jl0; jl < jl1; ++jl, ++gj) {
-    // prefetch row gj + 2
-    R2 z2, p2, W2;
-    if (jl + 1 < jl1) {
-      z2 = ldrow<BC>(z, g, col, gj + 2);
-      if (!first) p2 = ldrow<BC>(po, g, col, gj + 2);
-      if (KM) W2 = ldrow<BC_MIRROR>(op.w, g, col, gj + 2);
-    }
-    double2 ac = make_double2(0.0, 0.0), xo = make_double2(0.0, 0.0), poc = make_double2(0.0, 0.0);
-    const size_t o = off(g, gj, col.cc);
-    if (AM) ac = *reinterpret_cast<const double2*>(op.a + o);
-    if (!first) {
-      xo = *reinterpret_cast<const double2*>(x + o);
-      poc = *reinterpret_cast<const double2*>(po + o);
-    }
-    const R2 Pp = first ? z1 : comb(z1, p1);
+  for (int k = 0; k < n; ++k, gj += DIR) {
+    if (k + 1 < n) load_rawA<BC, AM, KM>(r2, g, col, op, z, po, x, gj + 2 * DIR, first, k + 2 < n);
+    const R2 Pa = comb(r1);
     double pw = P0.w, pe = P0.e;
     xnb(col, P0.v, pw, pe);
     double ww = 0.0, we = 0.0;
@@ -419,86 +425,93 @@ __global__ void __launch_bounds__(128) k_cg5_A2(Geom g, Op5 op, const double* __
       we = W0.e;
       xnb(col, W0.v, ww, we);
     }
+    const R2& Ps = DIR > 0 ? Pb : Pa;   // south (j-1), north (j+1)
+    const R2& Pn = DIR > 0 ? Pa : Pb;
+    const double2 ws = DIR > 0 ? Wb.v : r1.w.v;
+    const double2 wn = DIR > 0 ? r1.w.v : Wb.v;
     double2 y, d;
-    eval_pair<BC, AM, KM>(op, g, gj, ac, W0.v, ww, we, Wm.v, W1.v, P0.v, pw, pe, Pm.v, Pp.v, y, d);
+    eval_pair<BC, AM, KM>(op, g, gj, r0.a, W0.v, ww, we, ws, wn, P0.v, pw, pe, Ps.v, Pn.v, y, d);
     if (col.act) {
+      const size_t o = off(g, gj, col.cc);
       *reinterpret_cast<double2*>(pn + o) = P0.v;
       if (!first) {
-        xo.x += alpha * poc.x;
-        xo.y += alpha * poc.y;
+        double2 xo = r0.x;
+        xo.x += alpha * r0.p.v.x;
+        xo.y += alpha * r0.p.v.y;
         *reinterpret_cast<double2*>(x + o) = xo;
       }
       acc += P0.v.x * y.x + P0.v.y * y.y;
     }
-    Pm = P0;
-    P0 = Pp;
-    z1 = z2;
-    p1 = first ? z2 : p2;
-    if (KM) {
-      Wm = W0;
-      W0 = W1;
-      W1 = W2;
-    }
+    Pb = P0;
+    P0 = Pa;
+    Wb = W0;
+    W0 = r1.w;
+    r0 = r1;
+    r1 = r2;
   }
   double v[1] = {acc};
   block_reduce_finalize<1>(v, ra);
 }
 
-// B: r = d z - alpha A p; z = r / d; reduce (r, z), (r, r)
+struct RawB {
+  R2 p, w;
+  double2 z, a;
+};
+
 template <int BC, int AM, int KM>
-__global__ void __launch_bounds__(128) k_cg5_B2(Geom g, Op5 op, const double* __restrict__ p,
-                                                double* __restrict__ z, int strip, int reverse,
-                                                RedArgs ra) {
+__device__ __forceinline__ void load_rawB(RawB& r, const Geom& g, const Col2& col, const Op5& op,
+                                          const double* __restrict__ p,
+                                          const double* __restrict__ z, int gj, bool centre) {
+  r.p = ldrow<BC>(p, g, col, gj);
+  if (KM) r.w = ldrow<BC_MIRROR>(op.w, g, col, gj);
+  if (centre) {
+    const size_t o = off(g, gj, col.cc);
+    r.z = *reinterpret_cast<const double2*>(z + o);
+    if (AM) r.a = *reinterpret_cast<const double2*>(op.a + o);
+  }
+}
+
+// B: r = d z - alpha A p; z = r / d; reduce (r, z), (r, r)
+template <int BC, int AM, int KM, int DIR>
+__global__ void __launch_bounds__(128) k_cg5_B3(Geom g, Op5 op, const double* __restrict__ p,
+                                                double* __restrict__ z, int strip, RedArgs ra) {
   if (ra.sc->done) return;
   const double alpha = ra.sc->alpha;
   const Col2 col(g);
-  const int by = reverse ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y;
-  const int jl0 = by * strip, jl1 = min(jl0 + strip, g.nyl);
-  int gj = g.j0 + jl0;
-  R2 Pm = ldrow<BC>(p, g, col, gj - 1), P0 = ldrow<BC>(p, g, col, gj),
-     P1 = ldrow<BC>(p, g, col, gj + 1);
-  R2 Wm, W0, W1;
-  if (KM) {
-    Wm = ldrow<BC_MIRROR>(op.w, g, col, gj - 1);
-    W0 = ldrow<BC_MIRROR>(op.w, g, col, gj);
-    W1 = ldrow<BC_MIRROR>(op.w, g, col, gj + 1);
-  }
+  const int jl0 = blockIdx.y * strip, jl1 = min(jl0 + strip, g.nyl);
+  const int jb = DIR > 0 ? jl0 : jl1 - 1;
+  const int n = jl1 - jl0;
+  RawB rb, r0, r1, r2;
+  int gj = g.j0 + jb;
+  load_rawB<BC, AM, KM>(rb, g, col, op, p, z, gj - DIR, false);
+  load_rawB<BC, AM, KM>(r0, g, col, op, p, z, gj, true);
+  load_rawB<BC, AM, KM>(r1, g, col, op, p, z, gj + DIR, n > 1);
   double s0 = 0.0, s1 = 0.0;
-  for (int jl = jl0; jl < jl1; ++jl, ++gj) {
-    R2 P2, W2;
-    if (jl + 1 < jl1) {
-      P2 = ldrow<BC>(p, g, col, gj + 2);
-      if (KM) W2 = ldrow<BC_MIRROR>(op.w, g, col, gj + 2);
-    }
-    const size_t o = off(g, gj, col.cc);
-    double2 ac = make_double2(0.0, 0.0);
-    if (AM) ac = *reinterpret_cast<const double2*>(op.a + o);
-    const double2 zc = *reinterpret_cast<const double2*>(z + o);
-    double pw = P0.w, pe = P0.e;
-    xnb(col, P0.v, pw, pe);
+  for (int k = 0; k < n; ++k, gj += DIR) {
+    if (k + 1 < n) load_rawB<BC, AM, KM>(r2, g, col, op, p, z, gj + 2 * DIR, k + 2 < n);
+    double pw = r0.p.w, pe = r0.p.e;
+    xnb(col, r0.p.v, pw, pe);
     double ww = 0.0, we = 0.0;
     if (KM) {
-      ww = W0.w;
-      we = W0.e;
-      xnb(col, W0.v, ww, we);
+      ww = r0.w.w;
+      we = r0.w.e;
+      xnb(col, r0.w.v, ww, we);
     }
+    const double2 ps = DIR > 0 ? rb.p.v : r1.p.v, pnn = DIR > 0 ? r1.p.v : rb.p.v;
+    const double2 ws = DIR > 0 ? rb.w.v : r1.w.v, wn = DIR > 0 ? r1.w.v : rb.w.v;
     double2 y, d;
-    eval_pair<BC, AM, KM>(op, g, gj, ac, W0.v, ww, we, Wm.v, W1.v, P0.v, pw, pe, Pm.v, P1.v, y, d);
+    eval_pair<BC, AM, KM>(op, g, gj, r0.a, r0.w.v, ww, we, ws, wn, r0.p.v, pw, pe, ps, pnn, y, d);
     if (col.act) {
-      const double rx = d.x * zc.x - alpha * y.x, ry = d.y * zc.y - alpha * y.y;
+      const size_t o = off(g, gj, col.cc);
+      const double rx = d.x * r0.z.x - alpha * y.x, ry = d.y * r0.z.y - alpha * y.y;
       const double2 zn = make_double2(rx / d.x, ry / d.y);
       *reinterpret_cast<double2*>(z + o) = zn;
       s0 += rx * zn.x + ry * zn.y;
       s1 += rx * rx + ry * ry;
     }
-    Pm = P0;
-    P0 = P1;
-    P1 = P2;
-    if (KM) {
-      Wm = W0;
-      W0 = W1;
-      W1 = W2;
-    }
+    rb = r0;
+    r0 = r1;
+    r1 = r2;
   }
   double v[2] = {s0, s1};
   block_reduce_finalize<2>(v, ra);
@@ -540,6 +553,13 @@ __global__ void __launch_bounds__(256) k_sub_mean(Geom g, double* __restrict__ x
 
 __global__ void k_finalize_slabs(const double* tot, int nslabs, int K, RedArgs ra) {
   if (threadIdx.x != 0) return;
+  // iteration-phase finalizers are no-ops once the solve is done (their slab
+  // kernels returned early and the totals are stale); BiCGStab's omega phase
+  // is skipped after a half-step convergence
+  const int iter_phase = ra.fin == FIN_CG_A || ra.fin == FIN_CG_B || ra.fin == FIN_BI_ALPHA ||
+                         ra.fin == FIN_BI_S || ra.fin == FIN_BI_OMEGA || ra.fin == FIN_BI_R;
+  if (iter_phase && ra.sc->done) return;
+  if (ra.fin == FIN_BI_OMEGA && ra.sc->half) return;
   double t[8];
   for (int k = 0; k < K; ++k) {
     double s = 0.0;
@@ -583,17 +603,56 @@ void launch_cg5_init(const OpDesc& d, const Geom& g, const double* x, const doub
                            g, op, x, b, use_shift, z, strip, ra)));
 }
 
+// One resident wave: strip height chosen so that (column blocks x strips)
+// fits the occupancy of the kernel instance on this device.
+template <typename K>
+static int wave_strip(K kern, const Geom& g, int min_strip) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0);
+  if (per_sm < 1) per_sm = 1;
+  const int cap = nsm * per_sm;
+  const int ncb = (g.nx + 255) / 256;
+  int nstrips = cap / ncb;
+  if (nstrips < 1) nstrips = 1;
+  int strip = (g.nyl + nstrips - 1) / nstrips;
+  if (strip < min_strip) strip = min_strip;
+  return strip;
+}
+
 static dim3 grid5v(const Geom& g, int strip) {
   return dim3((g.nx + 255) / 256, (g.nyl + strip - 1) / strip);
+}
+
+template <int BC, int AM, int KM>
+static void launch_A3(const OpDesc& d, const Op5& op, const Geom& g, const double* z,
+                      const double* po, double* pn, double* x, int first, const RedArgs& ra,
+                      cudaStream_t st) {
+  const int strip = d.strip2 > 0 ? d.strip2 : wave_strip(k_cg5_A3<BC, AM, KM, 1>, g, 2);
+  k_cg5_A3<BC, AM, KM, 1><<<grid5v(g, strip), 128, 0, st>>>(g, op, z, po, pn, x, first, strip, ra);
+}
+
+template <int BC, int AM, int KM>
+static void launch_B3(const OpDesc& d, const Op5& op, const Geom& g, const double* p, double* z,
+                      const RedArgs& ra, cudaStream_t st) {
+  const int strip = d.strip2 > 0 ? d.strip2 : wave_strip(k_cg5_A3<BC, AM, KM, 1>, g, 2);
+  k_cg5_B3<BC, AM, KM, -1><<<grid5v(g, strip), 128, 0, st>>>(g, op, p, z, strip, ra);
 }
 
 void launch_cg5_A(const OpDesc& d, const Geom& g, const double* z, const double* po, double* pn,
                   double* x, int first, const RedArgs& ra, cudaStream_t st) {
   const Op5 op = make_op(d);
+  if (d.vec == 2 && (g.nx % 2 == 0)) {
+    launch_cg5_A_tma(d, g, z, po, pn, x, first, ra, st);
+    return;
+  }
   if (d.vec && (g.nx % 2 == 0)) {
-    const int strip = d.strip2;
-    CHB_DISPATCH(d.kind, (k_cg5_A2<BC, AM, KM><<<grid5v(g, strip), 128, 0, st>>>(
-                             g, op, z, po, pn, x, first, strip, 0, ra)));
+    CHB_DISPATCH(d.kind, (launch_A3<BC, AM, KM>(d, op, g, z, po, pn, x, first, ra, st)));
     return;
   }
   const int strip = d.strip;
@@ -604,10 +663,12 @@ void launch_cg5_A(const OpDesc& d, const Geom& g, const double* z, const double*
 void launch_cg5_B(const OpDesc& d, const Geom& g, const double* p, double* z, const RedArgs& ra,
                   cudaStream_t st) {
   const Op5 op = make_op(d);
+  if (d.vec == 2 && (g.nx % 2 == 0)) {
+    launch_cg5_B_tma(d, g, p, z, ra, st);
+    return;
+  }
   if (d.vec && (g.nx % 2 == 0)) {
-    const int strip = d.strip2;
-    CHB_DISPATCH(d.kind, (k_cg5_B2<BC, AM, KM><<<grid5v(g, strip), 128, 0, st>>>(
-                             g, op, p, z, strip, 1, ra)));
+    CHB_DISPATCH(d.kind, (launch_B3<BC, AM, KM>(d, op, g, p, z, ra, st)));
     return;
   }
   const int strip = d.strip;

@@ -49,6 +49,11 @@ void launch_cg5_A(const OpDesc& d, const Geom& g, const double* z, const double*
                   double* x, int first, const RedArgs& ra, cudaStream_t st);
 void launch_cg5_B(const OpDesc& d, const Geom& g, const double* p, double* z, const RedArgs& ra,
                   cudaStream_t st);
+// TMA-staged variants (kernels_cg5_tma.cu), even nx only
+void launch_cg5_A_tma(const OpDesc& d, const Geom& g, const double* z, const double* po,
+                      double* pn, double* x, int first, const RedArgs& ra, cudaStream_t st);
+void launch_cg5_B_tma(const OpDesc& d, const Geom& g, const double* p, double* z,
+                      const RedArgs& ra, cudaStream_t st);
 void launch_op5_apply(const OpDesc& d, const Geom& g, const double* x, double* y,
                       cudaStream_t st);
 void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace,

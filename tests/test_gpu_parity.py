@@ -209,3 +209,24 @@ def test_mass_conserved_and_divergence_free_on_gpu():
         d = ex.divergence(g["u"], g["v"])
         assert np.abs(d).max() < 1e-6
     sim.close()
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "2"])
+@pytest.mark.parametrize("nx,ny", [(64, 48), (300, 70)])
+def test_cg_kernel_variants_match_oracle(variant, nx, ny, monkeypatch):
+    """Scalar (0), register-pipelined vector (1) and TMA-ring (2) CG kernels,
+    including a ragged chunk (nx = 300: 256 + 44 columns)."""
+    monkeypatch.setenv("CHB_VEC", variant)
+    got, ref, st, iters = _run_both(nx, ny, 1)
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (variant, k, _rel(got[k], ref[k]))
+
+
+@pytest.mark.parametrize("variant", ["1", "2"])
+def test_cg_kernel_variants_short_strips(variant, monkeypatch):
+    """Forced 3-row strips: many strips per slab, halo rows at every strip edge."""
+    monkeypatch.setenv("CHB_VEC", variant)
+    monkeypatch.setenv("CHB_STRIP", "3")
+    got, ref, _, _ = _run_both(64, 40, 1)
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (variant, k, _rel(got[k], ref[k]))
