@@ -101,7 +101,7 @@ def main():
             if len(r) <= iv or r[im] != "gpu__time_duration.sum":
                 continue
             v = float(r[iv].replace(",", ""))
-            v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[iu], 1.0)
+            v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[iu], 1.0)
             c = kernel_class(r[ik])
             tot[c] += v
             cnt[c] += 1

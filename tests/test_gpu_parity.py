@@ -49,10 +49,48 @@ def _run_both(nx, ny, steps, seed=0, slabs=1, **over):
     return got, ref, st, iters
 
 
+def _oracle_truncation(nx, ny, seed=0, steps=1, **over):
+    """Relative L2 distance, per field, between the oracle's step at the run's
+    rtol and the same step solved to rtol 1e-13: how far the solution itself
+    moves with the solver's stopping point (oracle only, no GPU input)."""
+    from paper_1811_11842_b200 import SimParams
+    from oracle import initial_state, step
+    from workloads import initial_fields
+    f = initial_fields(nx, ny, seed=seed)
+    sp = SimParams(**over)
+    a = b = initial_state(f)
+    for _ in range(steps):
+        a, _ = step(a, _oracle_params(sp))
+        b, _ = step(b, _oracle_params(sp, rtol=1e-13))
+    return {k: _rel(getattr(a, k), getattr(b, k)) for k in FIELDS}
+
+
 @pytest.mark.parametrize("nx,ny", [(64, 64), (50, 37), (130, 70)])
 def test_one_step_matches_oracle(nx, ny):
-    got, ref, st, iters = _run_both(nx, ny, 1)
+    """Element-by-element parity, north_star bound 1e-9 on every field.  The
+    solves run to rtol 1e-12 on both sides (<= north_star's 1e-10): at 1e-10
+    the projected v is only determined to ~2e-7 by the stopping point itself
+    (R17), so a 1e-9 comparison there would test the stopping
+    iteration, not the arithmetic."""
+    got, ref, st, iters = _run_both(nx, ny, 1, rtol=1e-12)
     for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
+    for sysname, n in iters[-1].items():
+        assert abs(st["iters_last"][sysname] - n) <= 2, (sysname, st["iters_last"], iters[-1])
+        assert st["resid_last"][sysname] <= 1e-12
+
+
+@pytest.mark.parametrize("nx,ny", [(64, 64), (130, 70)])
+def test_one_step_at_north_star_rtol(nx, ny):
+    """At north_star's rtol 1e-10 every field matches within 1e-9 plus the
+    oracle's own stopping-point sensitivity (R17), the iteration counts agree
+    within 2 and every solve reaches 1e-10."""
+    got, ref, st, iters = _run_both(nx, ny, 1)
+    tr = _oracle_truncation(nx, ny)
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9 + tr[k], (k, _rel(got[k], ref[k]), tr[k])
+    for k in ("phi", "c", "u"):
+        assert tr[k] < 1e-9
         assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
     for sysname, n in iters[-1].items():
         assert abs(st["iters_last"][sysname] - n) <= 2, (sysname, st["iters_last"], iters[-1])
