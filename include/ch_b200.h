@@ -133,7 +133,8 @@ enum {
   CH_KC_VEC = 4,      /* fused BLAS-1 + reductions (BiCGStab / GMRES updates)                */
   CH_KC_RHS = 5,      /* explicit right-hand sides, coefficients, projection                 */
   CH_KC_GMRES = 6,    /* GMRES orthogonalisation                                            */
-  CH_NKC = 7
+  CH_KC_CG_FUSED = 7, /* single-reduction CG: one fused sweep per iteration (default CG path)  */
+  CH_NKC = 8
 };
 
 /* Create a handle: allocates the rank's slab state and workspace on
@@ -172,6 +173,18 @@ int ch_get_field(ch_handle* h, int field, double* dst, int where);
 /* Isolated matrix-free apply y = Op x on the local slab (halo exchange
  * included for multi-slab handles), coefficients from the current state. */
 int ch_apply_operator(ch_handle* h, int op, const double* x, double* y, int where);
+
+/* Isolated solve Op x = b on the local slab with the operator's coefficients
+ * from the current state and the step's Krylov method for that operator
+ * (CH_OP_CH: BiCGStab or GMRES(m) per params.ch_solver, PAPER.md:233-244;
+ * the 5-point operators: Jacobi-preconditioned CG; for
+ * CH_OP_POISSON b is projected to mean zero and x returned with mean zero,
+ * Listing 5).  x: initial guess in, solution out (nrows x nx, same `where`
+ * as b).  Stops at ||r||_2 <= rtol ||b||_2 (R13); the iteration count and
+ * final residual land in ch_stats.{iters_last,resid_last}[system]
+ * (CH_SYS_CH, CH_SYS_P, CH_SYS_U, CH_SYS_V).  Returns CH_ERR_NOT_CONVERGED /
+ * CH_ERR_BREAKDOWN like ch_step.  Does not advance the state. */
+int ch_solve(ch_handle* h, int op, const double* b, double* x, int where);
 
 int ch_get_stats(const ch_handle* h, ch_stats* out);
 int ch_reset_stats(ch_handle* h);

@@ -162,6 +162,21 @@ class Simulation:
         self._check(lib.ch_apply_operator(self._h, _lib.OPS[op], px, py, wx))
         return y
 
+    def solve(self, op: str, b, x0=None):
+        """Solve Op x = b (coefficients from the current state) with the step's
+        Krylov method for that operator; returns x (same kind of array as b)."""
+        import copy as _copy
+        if x0 is None:
+            x = np.zeros_like(b) if isinstance(b, np.ndarray) else _copy.copy(b).new_zeros(b.shape)
+        else:
+            x = x0.copy() if isinstance(x0, np.ndarray) else x0.clone()
+        pb, wb = _ptr(b, self.shape)
+        px, wx = _ptr(x, self.shape)
+        if wb != wx:
+            raise ValueError("b and x0 must both be host or both be device arrays")
+        self._check(lib.ch_solve(self._h, _lib.OPS[op], pb, px, wb))
+        return x
+
     # -- stats / timing
     def enable_timing(self, stride: int = 1):
         self._check(lib.ch_enable_timing(self._h, stride))

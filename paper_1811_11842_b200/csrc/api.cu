@@ -75,8 +75,10 @@ struct ch_handle {
   size_t arr_elems = 0;
   double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
   double* gm_host = nullptr;  // pinned mirror
-  int vec = 2;                // CG kernels: 2 TMA ring, 1 register pipeline, 0 scalar (env CHB_VEC)
+  int vec = 3;                // CG: 3 single-reduction fused TMA sweep; two-kernel HS-CG with
+                              // 2 TMA ring, 1 register pipeline, 0 scalar (env CHB_VEC)
   int strip2 = 0;             // rows per strip, 0 = one resident wave (env CHB_STRIP)
+  int pdl = 1;                // programmatic dependent launch of the CG sweeps (env CHB_PDL)
 };
 
 namespace {
@@ -288,6 +290,7 @@ OpDesc opdesc(ch_handle* h, int kind, const Slab& s) {
   d.strip = 16;
   d.strip2 = h->strip2;
   d.vec = h->vec;
+  d.pdl = h->pdl;
   d.a = nullptr;
   d.w = nullptr;
   d.s = 1.0;
@@ -359,7 +362,7 @@ int cg_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, i
     KTime kt(h, CH_KC_VEC, 24.0 * cells);
     for (int s = 0; s < h->S; ++s) {
       Slab& sl = h->sl[s];
-      launch_cg5_finish(sl.g, sl.a[xid], sl.a[plast], nullspace, rargs(h, FIN_MEAN, sys, s),
+      launch_cg5_finish(sl.g, sl.a[xid], sl.a[plast], nullspace, 0, rargs(h, FIN_MEAN, sys, s),
                         h->st);
     }
   }
@@ -367,6 +370,85 @@ int cg_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, i
   if (nullspace) TRY(fin_slabs(h, FIN_MEAN, sys, 1));
   harvest(h, K);
   return solve_status(h, sys, name);
+}
+
+// ------------------------------------------- single-reduction CG (default)
+// One fused sweep per iteration (kernels_cgs.cu).  Buffers: z ping-pong
+// (A_Z, A_R), s ping-pong (A_RH, A_BP), p in place (A_PA) -- the BiCGStab
+// work arrays are free while the symmetric systems are solved.
+int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, int use_shift,
+              const char* name, int wid = -1) {
+  TRY(set_maxit(h, sys));
+  const int AM = (kind == OPK_NUTRIENT || kind == OPK_MOM_U || kind == OPK_MOM_V);
+  if (wid >= 0) TRY(halo(h, wid, 2));
+  if (AM) TRY(halo(h, A_CA, 1));
+  TRY(halo(h, xid, 1));
+  const int Z[2] = {A_Z, A_R}, S[2] = {A_RH, A_BP}, P = A_PA;
+  const double cells = (double)h->grid.nx * (double)h->nrows / h->S;
+  {
+    KTime kt(h, CH_KC_CG_INIT, 40.0 * cells);
+    for (int s = 0; s < h->S; ++s) {
+      Slab& sl = h->sl[s];
+      launch_cg5_init(opdesc(h, kind, sl), sl.g, sl.a[xid], sl.a[bid], use_shift, sl.a[Z[0]],
+                      rargs(h, FIN_CG_INIT, sys, s), h->st);
+    }
+  }
+  TRY(check_launch(h, "cg5_init"));
+  TRY(fin_slabs(h, FIN_CG_INIT, sys, 3));
+  TRY(halo(h, Z[0], 2));
+  {
+    KTime kt(h, CH_KC_CG_INIT, 16.0 * cells);
+    for (int s = 0; s < h->S; ++s) {
+      Slab& sl = h->sl[s];
+      launch_cgs_delta0(opdesc(h, kind, sl), sl.g, sl.a[Z[0]], rargs(h, FIN_CGS_D0, sys, s),
+                        h->st);
+    }
+  }
+  TRY(check_launch(h, "cgs_delta0"));
+  TRY(fin_slabs(h, FIN_CGS_D0, sys, 1));
+  long k = 0;
+  int chunk = 4;
+  for (;;) {
+    for (int it = 0; it < chunk; ++it, ++k) {
+      const int first = (k == 0), xupd = (int)(k & 1), dir = (k & 1) ? -1 : 1;
+      const int zi = Z[k & 1], zo = Z[(k + 1) & 1], si = S[(k + 1) & 1], so = S[k & 1];
+      {
+        KTime kt(h, CH_KC_CG_FUSED, cgs_bytes(kind, first, xupd) * cells, k + 1);
+        for (int s = 0; s < h->S; ++s) {
+          Slab& sl = h->sl[s];
+          launch_cgs_iter(opdesc(h, kind, sl), sl.g, sl.a[zi], sl.a[zo], sl.a[si], sl.a[so],
+                          sl.a[P], sl.a[xid], first, xupd, dir, rargs(h, FIN_CGS, sys, s), h->st);
+        }
+      }
+      TRY(fin_slabs(h, FIN_CGS, sys, 3));
+      TRY(halo(h, zo, 2));
+      TRY(halo(h, so, 1));
+    }
+    TRY(check_launch(h, "cgs iteration"));
+    TRY(poll(h, sys));
+    if (h->sch[sys].done) break;
+    if (chunk < 64) chunk *= 2;
+  }
+  const long K = h->sch[sys].iter;
+  {
+    KTime kt(h, CH_KC_VEC, 24.0 * cells);
+    for (int s = 0; s < h->S; ++s) {
+      Slab& sl = h->sl[s];
+      launch_cg5_finish(sl.g, sl.a[xid], sl.a[P], nullspace, 1, rargs(h, FIN_MEAN, sys, s),
+                        h->st);
+    }
+  }
+  TRY(check_launch(h, "cg5_finish"));
+  if (nullspace) TRY(fin_slabs(h, FIN_MEAN, sys, 1));
+  harvest(h, K);
+  return solve_status(h, sys, name);
+}
+
+int cg_any(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, int use_shift,
+           const char* name, int wid = -1) {
+  if (h->vec == 3 && (h->grid.nx % 2 == 0))
+    return cgs_solve(h, sys, kind, xid, bid, nullspace, use_shift, name, wid);
+  return cg_solve(h, sys, kind, xid, bid, nullspace, use_shift, name, wid);
 }
 
 // ------------------------------------------------------------ BiCGStab (CH)
@@ -465,6 +547,11 @@ int bicgstab_solve(ch_handle* h, int sys, int xid, int bid) {
 
 int gmres_solve(ch_handle* h, int sys, int xid, int bid);  // below
 
+int bicgstab_or_gmres(ch_handle* h, int xid, int bid) {
+  if (h->prm.ch_solver == CH_SOLVER_GMRES) return gmres_solve(h, CH_SYS_CH, xid, bid);
+  return bicgstab_solve(h, CH_SYS_CH, xid, bid);
+}
+
 // ------------------------------------------------------------- one step
 int step_once(ch_handle* h) {
   const Phys ph = phys(h->prm);
@@ -483,10 +570,7 @@ int step_once(ch_handle* h) {
   TRY(halo(h, A_PHIS, 2));
   TRY(halo(h, A_DINV, 2));
   TRY(copy_arr(h, A_PHIS, A_PHI1));
-  if (h->prm.ch_solver == CH_SOLVER_GMRES)
-    TRY(gmres_solve(h, CH_SYS_CH, A_PHI1, A_B));
-  else
-    TRY(bicgstab_solve(h, CH_SYS_CH, A_PHI1, A_B));
+  TRY(bicgstab_or_gmres(h, A_PHI1, A_B));
   // 2. nutrient
   TRY(halo(h, A_PHI1, 1));
   {
@@ -496,7 +580,7 @@ int step_once(ch_handle* h) {
   }
   TRY(check_launch(h, "nut_rhs"));
   TRY(copy_arr(h, A_C, A_C1));
-  TRY(cg_solve(h, CH_SYS_NUTRIENT, OPK_NUTRIENT, A_C1, A_B, 0, 0, "nutrient", A_CW));
+  TRY(cg_any(h, CH_SYS_NUTRIENT, OPK_NUTRIENT, A_C1, A_B, 0, 0, "nutrient", A_CW));
   // 3. intermediate velocity
   {
     KTime kt(h, CH_KC_RHS, 40.0 * cells);
@@ -504,14 +588,14 @@ int step_once(ch_handle* h) {
   }
   TRY(check_launch(h, "mom_rhs_u"));
   TRY(copy_arr(h, A_U, A_US));
-  TRY(cg_solve(h, CH_SYS_U, OPK_MOM_U, A_US, A_B, 0, 0, "momentum-u"));
+  TRY(cg_any(h, CH_SYS_U, OPK_MOM_U, A_US, A_B, 0, 0, "momentum-u"));
   {
     KTime kt(h, CH_KC_RHS, 40.0 * cells);
     for (auto& s : h->sl) launch_mom_rhs_v(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_B], h->st);
   }
   TRY(check_launch(h, "mom_rhs_v"));
   TRY(copy_arr(h, A_V, A_VS));
-  TRY(cg_solve(h, CH_SYS_V, OPK_MOM_V, A_VS, A_B, 0, 0, "momentum-v"));
+  TRY(cg_any(h, CH_SYS_V, OPK_MOM_V, A_VS, A_B, 0, 0, "momentum-v"));
   // 4. pressure Poisson with the constant null space
   TRY(halo(h, A_US, 1));
   TRY(halo(h, A_VS, 1));
@@ -525,7 +609,7 @@ int step_once(ch_handle* h) {
   TRY(check_launch(h, "div"));
   TRY(fin_slabs(h, FIN_MEAN, CH_SYS_P, 1));
   const int pk = (h->prm.rho_n == h->prm.rho_s) ? OPK_POISSON_CONST : OPK_POISSON_VAR;
-  TRY(cg_solve(h, CH_SYS_P, pk, A_P, A_B, 1, 1, "pressure", pk == OPK_POISSON_VAR ? A_PHI1 : -1));
+  TRY(cg_any(h, CH_SYS_P, pk, A_P, A_B, 1, 1, "pressure", pk == OPK_POISSON_VAR ? A_PHI1 : -1));
   {
     KTime kt(h, CH_KC_VEC, 16.0 * cells);
     for (auto& s : h->sl) launch_sub_mean(s.g, s.a[A_P], h->sc + CH_SYS_P, h->st);
@@ -830,6 +914,7 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   h->nslabs_total = total;
   if (const char* e = getenv("CHB_VEC")) h->vec = atoi(e);
   if (const char* e = getenv("CHB_STRIP")) h->strip2 = std::max(0, atoi(e));
+  if (const char* e = getenv("CHB_PDL")) h->pdl = atoi(e) != 0;
   memset(&h->stats, 0, sizeof(ch_stats));
   // rows: balanced split of ny over `total` slabs (first ny % total get one more)
   const int base = G.ny / total, rem = G.ny % total;
@@ -969,8 +1054,10 @@ int ch_step(ch_handle* h, int nsteps) {
   return CH_OK;
 }
 
-int ch_apply_operator(ch_handle* h, int op, const double* x, double* y, int where) {
-  if (!h || !x || !y) return CH_ERR_ARG;
+namespace {
+// Coefficients of operator `op` from the current state (what ch_step would
+// use for its first solve of that kind); returns the 5-point kind or -1 (CH).
+int prep_operator(ch_handle* h, int op, int* kind) {
   const Phys ph = phys(h->prm);
   TRY(halo(h, A_PHI, 2));
   TRY(halo(h, A_PHIP, 2));
@@ -979,42 +1066,81 @@ int ch_apply_operator(ch_handle* h, int op, const double* x, double* y, int wher
   TRY(halo(h, A_C, 1));
   for (auto& s : h->sl) launch_ch_rhs(s.g, ph, state(s), s.a[A_PHIS], s.a[A_DINV], s.a[A_TMP2], h->st);
   TRY(halo(h, A_PHIS, 2));
-  TRY(put(h, A_TMP, x, where));
+  TRY(halo(h, A_DINV, 2));
   switch (op) {
     case CH_OP_CH:
-      TRY(halo(h, A_TMP, 2));
-      for (int s = 0; s < h->S; ++s) {
-        Slab& sl = h->sl[s];
-        launch_ch_apply(sl.g, chcoef(h, sl, false), sl.a[A_TMP], sl.a[A_B], 0, nullptr, nullptr,
-                        0, 0, rargs(h, FIN_NONE, CH_NSYS, s), h->st);
-      }
+      *kind = -1;
       break;
-    case CH_OP_POISSON: {
+    case CH_OP_POISSON:
       TRY(copy_arr(h, A_PHI, A_PHI1));
-      TRY(halo(h, A_TMP, 1));
-      const int pk = (h->prm.rho_n == h->prm.rho_s) ? OPK_POISSON_CONST : OPK_POISSON_VAR;
-      for (auto& s : h->sl) launch_op5_apply(opdesc(h, pk, s), s.g, s.a[A_TMP], s.a[A_B], h->st);
+      *kind = (h->prm.rho_n == h->prm.rho_s) ? OPK_POISSON_CONST : OPK_POISSON_VAR;
       break;
-    }
     case CH_OP_MOM_U:
-    case CH_OP_MOM_V: {
-      TRY(halo(h, A_TMP, 1));
+    case CH_OP_MOM_V:
       for (auto& s : h->sl) {
         if (op == CH_OP_MOM_U)
           launch_mom_rhs_u(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_TMP2], h->st);
         else
           launch_mom_rhs_v(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_TMP2], h->st);
-        launch_op5_apply(opdesc(h, op == CH_OP_MOM_U ? OPK_MOM_U : OPK_MOM_V, s), s.g, s.a[A_TMP],
-                         s.a[A_B], h->st);
       }
+      *kind = (op == CH_OP_MOM_U) ? OPK_MOM_U : OPK_MOM_V;
       break;
-    }
     default:
       h->err = "bad operator id";
       return CH_ERR_ARG;
   }
+  return check_launch(h, "prep_operator");
+}
+}  // namespace
+
+int ch_apply_operator(ch_handle* h, int op, const double* x, double* y, int where) {
+  if (!h || !x || !y) return CH_ERR_ARG;
+  int kind = 0;
+  TRY(prep_operator(h, op, &kind));
+  TRY(put(h, A_TMP, x, where));
+  if (kind < 0) {
+    TRY(halo(h, A_TMP, 2));
+    for (int s = 0; s < h->S; ++s) {
+      Slab& sl = h->sl[s];
+      launch_ch_apply(sl.g, chcoef(h, sl, false), sl.a[A_TMP], sl.a[A_B], 0, nullptr, nullptr, 0,
+                      0, rargs(h, FIN_NONE, CH_NSYS, s), h->st);
+    }
+  } else {
+    TRY(halo(h, A_TMP, 1));
+    for (auto& s : h->sl) launch_op5_apply(opdesc(h, kind, s), s.g, s.a[A_TMP], s.a[A_B], h->st);
+  }
   TRY(check_launch(h, "apply_operator"));
   TRY(get(h, A_B, y, where));
+  if (where == CH_DEVICE) CK(cudaStreamSynchronize(h->st));
+  return CH_OK;
+}
+
+int ch_solve(ch_handle* h, int op, const double* b, double* x, int where) {
+  if (!h || !b || !x) return CH_ERR_ARG;
+  int kind = 0;
+  TRY(prep_operator(h, op, &kind));
+  TRY(put(h, A_B, b, where));
+  TRY(put(h, A_US, x, where));
+  int sys = CH_SYS_CH;
+  if (kind < 0) {
+    TRY(bicgstab_or_gmres(h, A_US, A_B));
+  } else {
+    sys = (op == CH_OP_POISSON) ? CH_SYS_P : (op == CH_OP_MOM_U ? CH_SYS_U : CH_SYS_V);
+    const int ns = (op == CH_OP_POISSON);
+    if (ns) {
+      for (int s = 0; s < h->S; ++s) {
+        Slab& sl = h->sl[s];
+        launch_sum(sl.g, sl.a[A_B], rargs(h, FIN_MEAN, sys, s), h->st);
+      }
+      TRY(check_launch(h, "sum"));
+      TRY(fin_slabs(h, FIN_MEAN, sys, 1));
+    }
+    TRY(cg_any(h, sys, kind, A_US, A_B, ns, ns, "solve",
+               kind == OPK_POISSON_VAR ? A_PHI1 : -1));
+    if (ns)
+      for (auto& s : h->sl) launch_sub_mean(s.g, s.a[A_US], h->sc + sys, h->st);
+  }
+  TRY(get(h, A_US, x, where));
   if (where == CH_DEVICE) CK(cudaStreamSynchronize(h->st));
   return CH_OK;
 }

@@ -90,7 +90,9 @@ enum Fin : int {
   FIN_BI_OMEGA,    // [t.s, t.t]
   FIN_BI_R,        // [r.r, rhat.r]
   FIN_MEAN,        // [sum]  -> mean = sum / ncells
-  FIN_STORE        // [v...] -> aux[k] = v[k]
+  FIN_STORE,       // [v...] -> aux[k] = v[k]
+  FIN_CGS_D0,      // [delta_0]                 single-reduction CG start
+  FIN_CGS          // [gamma, r.r, delta]       single-reduction CG iteration
 };
 
 struct FinCtx {
@@ -172,6 +174,30 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
     }
     case FIN_MEAN: {
       s->mean = t[0] / fc.ncells;
+      break;
+    }
+    case FIN_CGS_D0: {
+      if (s->done) break;
+      if (bad(t[0])) { s->status = 1; s->done = 1; break; }
+      s->alpha = s->rho / t[0];
+      s->beta = 0.0;
+      s->aux[0] = 0.0;
+      break;
+    }
+    case FIN_CGS: {
+      // Chronopoulos-Gear: beta = gamma'/gamma, alpha' = gamma'/(delta' - beta gamma'/alpha)
+      s->iter += 1;
+      s->rr = t[1];
+      if (t[1] <= s->tol2) { s->done = 1; break; }
+      if (s->iter >= s->maxit) { s->status = 2; s->done = 1; break; }
+      if (bad(t[0]) || bad(s->rho) || bad(s->alpha)) { s->status = 1; s->done = 1; break; }
+      const double beta = t[0] / s->rho;
+      const double den = t[2] - beta * t[0] / s->alpha;
+      if (bad(den)) { s->status = 1; s->done = 1; break; }
+      s->aux[0] = s->alpha;  // alpha_{i} for the deferred x update
+      s->beta = beta;
+      s->alpha = t[0] / den;
+      s->rho = t[0];
       break;
     }
     case FIN_STORE: {

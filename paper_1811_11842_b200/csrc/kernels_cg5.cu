@@ -520,12 +520,14 @@ __global__ void __launch_bounds__(128) k_cg5_B3(Geom g, Op5 op, const double* __
 // ---------------------------------------------------------------- CG finish
 // x += alpha p (last iteration's update, deferred by the A kernel), or x = 0
 // when b = 0; optional reduction of sum(x) for the null-space projection.
+// odd_only: the single-reduction CG defers x over pairs of sweeps, so only an
+// odd iteration count leaves the last alpha p pending.
 __global__ void __launch_bounds__(256) k_cg5_finish(Geom g, double* __restrict__ x,
                                                     const double* __restrict__ p, int nullspace,
-                                                    RedArgs ra) {
+                                                    int odd_only, RedArgs ra) {
   const KScal* sc = ra.sc;
   const int zero = sc->zero;
-  const int upd = (sc->iter >= 1) && !zero && sc->status == 0;
+  const int upd = (sc->iter >= 1) && !zero && sc->status == 0 && (!odd_only || (sc->iter & 1));
   const double alpha = sc->alpha;
   double acc = 0.0;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -556,7 +558,8 @@ __global__ void k_finalize_slabs(const double* tot, int nslabs, int K, RedArgs r
   // iteration-phase finalizers are no-ops once the solve is done (their slab
   // kernels returned early and the totals are stale); BiCGStab's omega phase
   // is skipped after a half-step convergence
-  const int iter_phase = ra.fin == FIN_CG_A || ra.fin == FIN_CG_B || ra.fin == FIN_BI_ALPHA ||
+  const int iter_phase = ra.fin == FIN_CG_A || ra.fin == FIN_CG_B || ra.fin == FIN_CGS ||
+                         ra.fin == FIN_CGS_D0 || ra.fin == FIN_BI_ALPHA ||
                          ra.fin == FIN_BI_S || ra.fin == FIN_BI_OMEGA || ra.fin == FIN_BI_R;
   if (iter_phase && ra.sc->done) return;
   if (ra.fin == FIN_BI_OMEGA && ra.sc->half) return;
@@ -689,9 +692,9 @@ static dim3 grid_pw(const Geom& g) {
   return dim3((g.nx + 255) / 256, gy);
 }
 
-void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace,
+void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace, int odd_only,
                        const RedArgs& ra, cudaStream_t st) {
-  k_cg5_finish<<<grid_pw(g), 256, 0, st>>>(g, x, p, nullspace, ra);
+  k_cg5_finish<<<grid_pw(g), 256, 0, st>>>(g, x, p, nullspace, odd_only, ra);
 }
 
 void launch_sub_mean(const Geom& g, double* x, const KScal* sc, cudaStream_t st) {

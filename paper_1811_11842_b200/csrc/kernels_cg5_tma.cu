@@ -14,79 +14,10 @@
 
 #include "common.cuh"
 #include "launch.h"
+#include "op5.cuh"
+#include "tma.cuh"
 
 namespace chb {
-
-// same face-coefficient / stencil definitions as kernels_cg5.cu (kept local:
-// the device functions are inlined per translation unit)
-struct Op5T {
-  const double* a;
-  const double* w;
-  double s, kscale, rho_n, rho_s;
-};
-
-template <int KM>
-__device__ __forceinline__ double kfaceT(const Op5T& op, double w1, double w2) {
-  if (KM == 0) return 1.0;
-  const double m = 0.5 * (w1 + w2);
-  if (KM == 1) return op.kscale * m;
-  return 1.0 / (op.rho_s + m * (op.rho_n - op.rho_s));
-}
-
-template <int BC, int AM, int KM>
-__device__ __forceinline__ void eval5T(const Op5T& op, const Geom& g, int gj, double ac, double wc,
-                                       double ww, double we, double ws, double wn, double xc,
-                                       double xw, double xe, double xs, double xn, double& y,
-                                       double& d) {
-  if (BC == BC_VFACE && gj == 0) {
-    y = xc;
-    d = 1.0;
-    return;
-  }
-  const double kE = kfaceT<KM>(op, wc, we), kW = kfaceT<KM>(op, ww, wc);
-  const double kN = kfaceT<KM>(op, wc, wn), kS = kfaceT<KM>(op, ws, wc);
-  double fS = 1.0, fN = 1.0;
-  if (BC == BC_MIRROR) {
-    fS = (gj == 0) ? 0.0 : 1.0;
-    fN = (gj == g.ny - 1) ? 0.0 : 1.0;
-  } else if (BC == BC_ODD) {
-    fS = (gj == 0) ? 2.0 : 1.0;
-    fN = (gj == g.ny - 1) ? 2.0 : 1.0;
-  }
-  const double a = AM ? ac : 0.0;
-  y = a * xc + op.s * ((kE * (xc - xe) + kW * (xc - xw)) * g.ihx2 +
-                       (kN * (xc - xn) + kS * (xc - xs)) * g.ihy2);
-  d = a + op.s * ((kE + kW) * g.ihx2 + (fN * kN + fS * kS) * g.ihy2);
-}
-
-// ------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t s_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(s_u32(dst)),
-      "l"(src), "r"(bytes), "r"(s_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(s_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
 
 constexpr int TW = 256;   // columns per block (128 threads x 2)
 constexpr int TSEG = TW + 4;
@@ -105,7 +36,7 @@ struct Streams {
 
 template <int BC>
 __device__ __forceinline__ int fold_src_row(const Geom& g, int gj) {
-  if (BC == BC_VFACE) return gj <= 0 ? 1 : (gj >= g.ny ? g.ny - 1 : gj);  // value ignored
+  if (BC == BC_VFACE) return gj < 0 ? 1 : (gj >= g.ny ? g.ny - 1 : gj);  // ghosts: value ignored
   if (gj < 0) return -1 - gj;
   if (gj >= g.ny) return 2 * g.ny - 1 - gj;
   return gj;
@@ -150,13 +81,6 @@ __device__ __forceinline__ void issue_row(const Geom& g, const Streams& S, doubl
   }
 }
 
-__device__ __forceinline__ void ring_setup(uint64_t* bars, int nst) {
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < nst; ++i) mbar_init(bars + i, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-}
 
 // sign / zero of a staged unknown value at global row gj (BC at read time)
 template <int BC>

@@ -20,6 +20,7 @@ struct OpDesc {
   int strip;          // rows per marching strip (scalar kernels)
   int strip2;         // rows per strip of the vectorised kernels
   int vec;            // use the 2-column vectorised kernels when nx is even
+  int pdl;            // programmatic dependent launch for the fused CG sweeps
   const double* a;    // diagonal coefficient array (NUTRIENT, MOM_*)
   const double* w;    // cell coefficient (NUTRIENT: phi_s^{1/2}; POISSON_VAR: phi^{n+1})
   double s, kscale, rho_n, rho_s;
@@ -56,8 +57,16 @@ void launch_cg5_B_tma(const OpDesc& d, const Geom& g, const double* p, double* z
                       const RedArgs& ra, cudaStream_t st);
 void launch_op5_apply(const OpDesc& d, const Geom& g, const double* x, double* y,
                       cudaStream_t st);
-void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace,
+void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace, int odd_only,
                        const RedArgs& ra, cudaStream_t st);
+// single-reduction CG (kernels_cgs.cu), even nx only
+void launch_cgs_iter(const OpDesc& d, const Geom& g, const double* zi, double* zo,
+                     const double* si, double* so, double* P, double* X, int first, int xupd,
+                     int dir, const RedArgs& ra, cudaStream_t st);
+void launch_cgs_delta0(const OpDesc& d, const Geom& g, const double* z, const RedArgs& ra,
+                       cudaStream_t st);
+double cgs_bytes(int kind, int first, int xupd);
+void launch_sum(const Geom& g, const double* x, const RedArgs& ra, cudaStream_t st);
 void launch_sub_mean(const Geom& g, double* x, const KScal* sc, cudaStream_t st);
 void launch_finalize_slabs(const double* tot, int nslabs, int K, const RedArgs& ra,
                            cudaStream_t st);
