@@ -26,7 +26,8 @@ enum Arr {
   A_Z, A_PA, A_PB,                         // CG
   A_R, A_RH, A_BP, A_BV, A_BS, A_BT,       // BiCGStab
   A_TMP, A_TMP2,
-  A_N
+  A_ZH0,                                   // z history of the deferred-p/x CG (CGM - 1 more)
+  A_N = A_ZH0 + CGM - 1
 };
 
 constexpr int MAX_BLOCKS = 1 << 17;
@@ -73,6 +74,8 @@ struct ch_handle {
   Timer tm;
   Comm* comm = nullptr;
   size_t arr_elems = 0;
+  double* cgtab = nullptr;    // deferred-p/x CG coefficient tables, device [NSC][2][CGT]
+  int cg_defer = 8;           // block length m (2..12) of the deferred p/x CG (env CHB_DEFER)
   double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
   double* gm_host = nullptr;  // pinned mirror
   int vec = 3;                // CG: 3 single-reduction fused TMA sweep; two-kernel HS-CG with
@@ -190,6 +193,9 @@ RedArgs rargs(ch_handle* h, int fin, int sys, int slab) {
   ra.sc = h->sc + sys;
   ra.fc.rtol2 = h->prm.rtol * h->prm.rtol;
   ra.fc.ncells = (double)h->grid.nx * (double)h->grid.ny;
+  ra.fc.tab = h->cgtab ? h->cgtab + (size_t)sys * 2 * CGT : nullptr;
+  ra.fc.m = h->cg_defer;
+  ra.fc.pad = 0;
   ra.fin = fin;
   ra.inline_fin = (h->nslabs_total == 1);
   ra.slab = slab;
@@ -383,24 +389,45 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   if (wid >= 0) TRY(halo(h, wid, 2));
   if (AM) TRY(halo(h, A_CA, 1));
   TRY(halo(h, xid, 1));
-  const int Z[2] = {A_Z, A_R}, S[2] = {A_RH, A_BP}, P = A_PA;
+  // z ring of m + 1 buffers (p/x deferred over blocks of m sweeps)
+  const int m = h->cg_defer;
+  const int NZ = m + 1;
+  int Zr[CGM + 1];
+  Zr[0] = A_Z;
+  Zr[1] = A_R;
+  for (int k = 2; k < NZ; ++k) Zr[k] = A_ZH0 + (k - 2);
+  const int S[2] = {A_RH, A_BP}, P = A_PA;
   const double cells = (double)h->grid.nx * (double)h->nrows / h->S;
+  const double* tab = h->cgtab + (size_t)sys * 2 * CGT;
+  auto px = [&](long k_last, int n, int write_p) -> int {
+    // z_k of iterations k_last - n + 1 .. k_last
+    const long k0 = k_last - n + 1;
+    KTime kt(h, CH_KC_VEC, 8.0 * (n + 4) * cells);
+    for (int s = 0; s < h->S; ++s) {
+      Slab& sl = h->sl[s];
+      ZList zl;
+      for (int j = 0; j < CGM; ++j) zl.z[j] = j < n ? sl.a[Zr[(k0 + j) % NZ]] : nullptr;
+      launch_cgs_px(sl.g, zl, n, k0 == 0, write_p, (int)(k_last + 1),
+                    tab + ((k_last / m) & 1) * CGT, h->sc + sys, sl.a[P], sl.a[xid], h->st);
+    }
+    return check_launch(h, "cgs_px");
+  };
   {
     KTime kt(h, CH_KC_CG_INIT, 40.0 * cells);
     for (int s = 0; s < h->S; ++s) {
       Slab& sl = h->sl[s];
-      launch_cg5_init(opdesc(h, kind, sl), sl.g, sl.a[xid], sl.a[bid], use_shift, sl.a[Z[0]],
+      launch_cg5_init(opdesc(h, kind, sl), sl.g, sl.a[xid], sl.a[bid], use_shift, sl.a[Zr[0]],
                       rargs(h, FIN_CG_INIT, sys, s), h->st);
     }
   }
   TRY(check_launch(h, "cg5_init"));
   TRY(fin_slabs(h, FIN_CG_INIT, sys, 3));
-  TRY(halo(h, Z[0], 2));
+  TRY(halo(h, Zr[0], 2));
   {
     KTime kt(h, CH_KC_CG_INIT, 16.0 * cells);
     for (int s = 0; s < h->S; ++s) {
       Slab& sl = h->sl[s];
-      launch_cgs_delta0(opdesc(h, kind, sl), sl.g, sl.a[Z[0]], rargs(h, FIN_CGS_D0, sys, s),
+      launch_cgs_delta0(opdesc(h, kind, sl), sl.g, sl.a[Zr[0]], rargs(h, FIN_CGS_D0, sys, s),
                         h->st);
     }
   }
@@ -410,19 +437,20 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   int chunk = 4;
   for (;;) {
     for (int it = 0; it < chunk; ++it, ++k) {
-      const int first = (k == 0), xupd = (int)(k & 1), dir = (k & 1) ? -1 : 1;
-      const int zi = Z[k & 1], zo = Z[(k + 1) & 1], si = S[(k + 1) & 1], so = S[k & 1];
+      const int first = (k == 0), dir = (k & 1) ? -1 : 1;
+      const int zi = Zr[k % NZ], zo = Zr[(k + 1) % NZ], si = S[(k + 1) & 1], so = S[k & 1];
       {
-        KTime kt(h, CH_KC_CG_FUSED, cgs_bytes(kind, first, xupd) * cells, k + 1);
+        KTime kt(h, CH_KC_CG_FUSED, cgs_bytes(kind, first) * cells, k + 1);
         for (int s = 0; s < h->S; ++s) {
           Slab& sl = h->sl[s];
           launch_cgs_iter(opdesc(h, kind, sl), sl.g, sl.a[zi], sl.a[zo], sl.a[si], sl.a[so],
-                          sl.a[P], sl.a[xid], first, xupd, dir, rargs(h, FIN_CGS, sys, s), h->st);
+                          first, dir, rargs(h, FIN_CGS, sys, s), h->st);
         }
       }
       TRY(fin_slabs(h, FIN_CGS, sys, 3));
       TRY(halo(h, zo, 2));
       TRY(halo(h, so, 1));
+      if ((k + 1) % m == 0) TRY(px(k, m, 1));
     }
     TRY(check_launch(h, "cgs iteration"));
     TRY(poll(h, sys));
@@ -430,12 +458,13 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
     if (chunk < 64) chunk *= 2;
   }
   const long K = h->sch[sys].iter;
+  if (K > 0 && K % m != 0) TRY(px(K - 1, (int)(K % m), 0));
   {
     KTime kt(h, CH_KC_VEC, 24.0 * cells);
     for (int s = 0; s < h->S; ++s) {
       Slab& sl = h->sl[s];
-      launch_cg5_finish(sl.g, sl.a[xid], sl.a[P], nullspace, 1, rargs(h, FIN_MEAN, sys, s),
-                        h->st);
+      launch_cg5_finish(sl.g, sl.a[xid], sl.a[P], nullspace, 2,
+                        rargs(h, FIN_MEAN, sys, s), h->st);
     }
   }
   TRY(check_launch(h, "cg5_finish"));
@@ -875,6 +904,7 @@ static void destroy_mem(ch_handle* h) {
   if (h->tot) cudaFree(h->tot);
   if (h->tot_local) cudaFree(h->tot_local);
   if (h->gm_dev) cudaFree(h->gm_dev);
+  if (h->cgtab) cudaFree(h->cgtab);
   if (h->gm_host) cudaFreeHost(h->gm_host);
   for (auto& r : h->tm.pending) {
     cudaEventDestroy(r.e0);
@@ -915,6 +945,7 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   if (const char* e = getenv("CHB_VEC")) h->vec = atoi(e);
   if (const char* e = getenv("CHB_STRIP")) h->strip2 = std::max(0, atoi(e));
   if (const char* e = getenv("CHB_PDL")) h->pdl = atoi(e) != 0;
+  if (const char* e = getenv("CHB_DEFER")) h->cg_defer = std::min(std::max(2, atoi(e)), CGM);
   memset(&h->stats, 0, sizeof(ch_stats));
   // rows: balanced split of ny over `total` slabs (first ny % total get one more)
   const int base = G.ny / total, rem = G.ny % total;
@@ -945,7 +976,9 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
     sl.g.ihx2 = (double)G.nx * G.nx;
     sl.g.ihy2 = (double)G.ny * G.ny;
     for (int i = 0; i < A_N; ++i) sl.a[i] = nullptr;
-    for (int i = 0; i < A_N; ++i) {
+    // z history: only the m - 1 buffers the chosen block length needs
+    const int n_alloc = A_ZH0 + std::max(0, h->cg_defer - 1);
+    for (int i = 0; i < n_alloc; ++i) {
       if (cudaMalloc(&sl.a[i], h->arr_elems * sizeof(double)) != cudaSuccess)
         return fail(CH_ERR_CUDA, h, "cudaMalloc (out of device memory?)");
       cudaMemset(sl.a[i], 0, h->arr_elems * sizeof(double));
@@ -958,6 +991,7 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
       cudaMalloc(&h->tot, (size_t)total * 8 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&h->tot_local, (size_t)total * 8 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&h->gm_dev, 192 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&h->cgtab, (size_t)NSC * 2 * CGT * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->gm_host, 192 * sizeof(double)) != cudaSuccess)
     return fail(CH_ERR_CUDA, h, "cudaMalloc (scalars)");
   cudaMemset(h->sc, 0, NSC * sizeof(KScal));

@@ -98,7 +98,39 @@ enum Fin : int {
 struct FinCtx {
   double rtol2;
   double ncells;
+  double* tab;   // single-reduction CG with deferred p/x: coefficient tables of
+                 // this system, [2][CGT] (block parity), see cgs_coef_update
+  int m;         // iterations per deferred p/x block (0: p/x updated in-sweep)
+  int pad;
 };
+
+// Deferred p/x of the single-reduction CG (kernels_cgs.cu).  Within a block of
+// m iterations i0..i0+m-1 the directions and iterates are linear in the
+// stored preconditioned residuals z_k:
+//   p_i     = sum_k PZ[k] z_k + CPP p_{i0-1}
+//   x_{i+1} = x_{i0} + sum_k CZ[k] z_k + CXP p_{i0-1}
+// and the table follows the textbook updates p_i = z_i + beta_i p_{i-1},
+// x_{i+1} = x_i + alpha_i p_i exactly (only the summation order of x differs).
+constexpr int CGM = 32;  // max block length
+constexpr int CGT = 80;  // table stride (>= 2 CGM + 3)
+enum { CG_PZ = 0, CG_CZ = CGM, CG_CPP = 2 * CGM, CG_CXP = 2 * CGM + 1, CG_N = 2 * CGM + 2 };
+
+__device__ inline void cgs_coef_update(double* tab, int m, int i, double alpha, double beta) {
+  if (!tab || m <= 0) return;
+  double* T = tab + ((i / m) & 1) * CGT;
+  const int j = i % m;
+  if (j == 0) {
+    for (int k = 0; k < CGM; ++k) T[CG_PZ + k] = T[CG_CZ + k] = 0.0;
+    T[CG_CPP] = 1.0;
+    T[CG_CXP] = 0.0;
+  }
+  for (int k = 0; k < j; ++k) T[CG_PZ + k] *= beta;
+  T[CG_CPP] *= beta;
+  T[CG_PZ + j] = 1.0;
+  for (int k = 0; k <= j; ++k) T[CG_CZ + k] += alpha * T[CG_PZ + k];
+  T[CG_CXP] += alpha * T[CG_CPP];
+  T[CG_N] = (double)(j + 1);
+}
 
 __device__ __forceinline__ bool bad(double x) { return !(x == x) || x == 0.0; }
 
@@ -182,6 +214,7 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
       s->alpha = s->rho / t[0];
       s->beta = 0.0;
       s->aux[0] = 0.0;
+      cgs_coef_update(fc.tab, fc.m, 0, s->alpha, 0.0);
       break;
     }
     case FIN_CGS: {
@@ -194,10 +227,11 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
       const double beta = t[0] / s->rho;
       const double den = t[2] - beta * t[0] / s->alpha;
       if (bad(den)) { s->status = 1; s->done = 1; break; }
-      s->aux[0] = s->alpha;  // alpha_{i} for the deferred x update
+      s->aux[0] = s->alpha;  // alpha_{i} for the in-sweep x update over pairs
       s->beta = beta;
       s->alpha = t[0] / den;
       s->rho = t[0];
+      cgs_coef_update(fc.tab, fc.m, s->iter, s->alpha, beta);
       break;
     }
     case FIN_STORE: {

@@ -520,14 +520,16 @@ __global__ void __launch_bounds__(128) k_cg5_B3(Geom g, Op5 op, const double* __
 // ---------------------------------------------------------------- CG finish
 // x += alpha p (last iteration's update, deferred by the A kernel), or x = 0
 // when b = 0; optional reduction of sum(x) for the null-space projection.
-// odd_only: the single-reduction CG defers x over pairs of sweeps, so only an
-// odd iteration count leaves the last alpha p pending.
+// mode 0: add the last alpha p; 1 (single-reduction CG, x over pairs of
+// sweeps): only after an odd iteration count; 2 (deferred p/x blocks, already
+// applied): no update, only the b = 0 case and the null-space sum.
 __global__ void __launch_bounds__(256) k_cg5_finish(Geom g, double* __restrict__ x,
                                                     const double* __restrict__ p, int nullspace,
                                                     int odd_only, RedArgs ra) {
   const KScal* sc = ra.sc;
   const int zero = sc->zero;
-  const int upd = (sc->iter >= 1) && !zero && sc->status == 0 && (!odd_only || (sc->iter & 1));
+  const int upd = (sc->iter >= 1) && !zero && sc->status == 0 && odd_only != 2 &&
+                  (!odd_only || (sc->iter & 1));
   const double alpha = sc->alpha;
   double acc = 0.0;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;

@@ -61,11 +61,16 @@ void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace,
                        const RedArgs& ra, cudaStream_t st);
 // single-reduction CG (kernels_cgs.cu), even nx only
 void launch_cgs_iter(const OpDesc& d, const Geom& g, const double* zi, double* zo,
-                     const double* si, double* so, double* P, double* X, int first, int xupd,
-                     int dir, const RedArgs& ra, cudaStream_t st);
+                     const double* si, double* so, int first, int dir, const RedArgs& ra,
+                     cudaStream_t st);
+struct ZList {
+  const double* z[CGM];
+};
+void launch_cgs_px(const Geom& g, const ZList& zl, int n, int first_block, int write_p, int need,
+                   const double* T, const KScal* sc, double* P, double* X, cudaStream_t st);
 void launch_cgs_delta0(const OpDesc& d, const Geom& g, const double* z, const RedArgs& ra,
                        cudaStream_t st);
-double cgs_bytes(int kind, int first, int xupd);
+double cgs_bytes(int kind, int first);
 void launch_sum(const Geom& g, const double* x, const RedArgs& ra, cudaStream_t st);
 void launch_sub_mean(const Geom& g, double* x, const KScal* sc, cudaStream_t st);
 void launch_finalize_slabs(const double* tot, int nslabs, int K, const RedArgs& ra,

@@ -54,11 +54,12 @@ struct Cf5 {
   double kE, kW, kN, kS, a, d;
 };
 
-template <int BC, int AM, int KM>
+// WALLS = false: caller guarantees gj is neither a wall row nor (v) row 0.
+template <int BC, int AM, int KM, bool WALLS = true>
 __device__ __forceinline__ Cf5 coef5(const Op5T& op, const Geom& g, int gj, double ac, double wc,
                                      double ww, double we, double ws, double wn) {
   Cf5 c;
-  if (BC == BC_VFACE && gj == 0) {
+  if (WALLS && BC == BC_VFACE && gj == 0) {
     c.kE = c.kW = c.kN = c.kS = c.a = 0.0;
     c.d = 1.0;
     return c;
@@ -68,10 +69,10 @@ __device__ __forceinline__ Cf5 coef5(const Op5T& op, const Geom& g, int gj, doub
   c.kN = kfaceT<KM>(op, wc, wn);
   c.kS = kfaceT<KM>(op, ws, wc);
   double fS = 1.0, fN = 1.0;
-  if (BC == BC_MIRROR) {
+  if (WALLS && BC == BC_MIRROR) {
     fS = (gj == 0) ? 0.0 : 1.0;
     fN = (gj == g.ny - 1) ? 0.0 : 1.0;
-  } else if (BC == BC_ODD) {
+  } else if (WALLS && BC == BC_ODD) {
     fS = (gj == 0) ? 2.0 : 1.0;
     fN = (gj == g.ny - 1) ? 2.0 : 1.0;
   }
@@ -80,10 +81,10 @@ __device__ __forceinline__ Cf5 coef5(const Op5T& op, const Geom& g, int gj, doub
   return c;
 }
 
-template <int BC>
+template <int BC, bool WALLS = true>
 __device__ __forceinline__ double apply5(const Cf5& c, const Op5T& op, const Geom& g, int gj,
                                          double xc, double xw, double xe, double xs, double xn) {
-  if (BC == BC_VFACE && gj == 0) return xc;
+  if (WALLS && BC == BC_VFACE && gj == 0) return xc;
   return c.a * xc + op.s * ((c.kE * (xc - xe) + c.kW * (xc - xw)) * g.ihx2 +
                             (c.kN * (xc - xn) + c.kS * (xc - xs)) * g.ihy2);
 }

@@ -1,7 +1,9 @@
-"""Per-kernel-class timing of full time steps (CUDA events inside the library).
+"""Per-kernel-class timing (CUDA events inside the library) of full time steps,
+or of isolated solves of one operator.
 
-    CHB_VEC=2 python scripts/kbench.py [--config 3] [--steps 1] [--warmup 1]
-Prints one JSON line: per class launches / avg ms / GB/s (algorithmic bytes), iterations.
+    CHB_DEFER=8 python scripts/kbench.py [--config 3] [--steps 1] [--warmup 1]
+    python scripts/kbench.py --solve poisson|mom_u|mom_v [--config 3]
+Prints one JSON line: per class launches / avg us / GB/s (algorithmic bytes), iterations.
 """
 import argparse
 import json
@@ -19,17 +21,32 @@ ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--warmup", type=int, default=1)
 ap.add_argument("--stride", type=int, default=4)
+ap.add_argument("--solve", default=None)
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 sim = Simulation(cfg["nx"], cfg["ny"], dt=cfg["dt"])
 sim.set_fields(**initial_fields(cfg["nx"], cfg["ny"], seed=0))
-sim.step(a.warmup)
-sim.reset_stats()
-sim.enable_timing(a.stride)
-sim.step(a.steps)
+if a.solve:
+    import torch
+    n, m = cfg["ny"], cfg["nx"]
+    g = torch.Generator(device="cuda").manual_seed(3)
+    b = torch.randn((n, m), dtype=torch.float64, device="cuda", generator=g)
+    if a.solve == "poisson":
+        b -= b.mean()
+    if a.solve == "mom_v":
+        b[0] = 0.0
+    sim.solve(a.solve, b)          # warm-up
+    sim.reset_stats()
+    sim.enable_timing(a.stride)
+    sim.solve(a.solve, b)
+else:
+    sim.step(a.warmup)
+    sim.reset_stats()
+    sim.enable_timing(a.stride)
+    sim.step(a.steps)
 st = sim.stats()
-out = {"variant": os.environ.get("CHB_VEC", "default"), "config": cfg["name"],
-       "iters": st["iters_last"], "kernels": {}}
+out = {"variant": os.environ.get("CHB_VEC", "default"), "defer": os.environ.get("CHB_DEFER", "8"),
+       "solve": a.solve, "config": cfg["name"], "iters": st["iters_last"], "kernels": {}}
 for k, v in st["kernels"].items():
     if v["timed"]:
         out["kernels"][k] = {"launches": v["launches"], "avg_us": 1e3 * v["ms"] / v["timed"],
