@@ -155,7 +155,8 @@ def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_1811_11842_b200 import SimParams, Simulation, unique_id
+    from paper_1811_11842_b200 import SimParams, Simulation
+    from paper_1811_11842_b200.distributed import max_over_ranks, share_unique_id
 
     torch.cuda.set_device(local_rank)
     if world > 1:
@@ -165,9 +166,7 @@ def run_ours(args, rank, world, local_rank):
     sp = SimParams(dt=cfg["dt"], ch_solver=args.ch_solver)
     sim = Simulation(nx, ny, sp, rank=rank, nranks=world, device=local_rank)
     if world > 1:
-        obj = [unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        sim.comm_init(obj[0])
+        sim.comm_init(share_unique_id(dist, rank))
     stream = torch.cuda.current_stream()
     sim.set_stream(stream)
     rows = (sim.row0, sim.row0 + sim.nrows)
@@ -195,10 +194,7 @@ def run_ours(args, rank, world, local_rank):
     ms = e0.elapsed_time(e1)
     sim.enable_timing(0)
     st = sim.stats()
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(dist, ms, device="cuda")
     value = args.steps / (ms_max / 1e3)
     ms_step = ms_max / args.steps
 
@@ -241,11 +237,9 @@ def run_ours(args, rank, world, local_rank):
             sim.get_field("phi_prev", hprev)
         barrier()
         dt = time.perf_counter() - t0
-        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt_max = max_over_ranks(dist, dt, device="cuda")
         nbytes = 6 * sim.nrows * nx * 8
-        e2e = {"value": e2e_steps / float(tt.item()), "unit": "time-steps/s",
+        e2e = {"value": e2e_steps / dt_max, "unit": "time-steps/s",
                "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world}
 
     cpu = None

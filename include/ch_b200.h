@@ -133,8 +133,12 @@ enum {
   CH_KC_VEC = 4,      /* fused BLAS-1 + reductions (BiCGStab / GMRES updates)                */
   CH_KC_RHS = 5,      /* explicit right-hand sides, coefficients, projection                 */
   CH_KC_GMRES = 6,    /* GMRES orthogonalisation                                            */
-  CH_KC_CG_FUSED = 7, /* single-reduction CG: one fused sweep per iteration (default CG path)  */
-  CH_NKC = 8
+  CH_KC_CG_FUSED = 7, /* single-reduction CG sweep, nutrient system (default CG path)         */
+  CH_KC_CG_FUSED_U = 8,  /* ... momentum u                                                   */
+  CH_KC_CG_FUSED_V = 9,  /* ... momentum v                                                   */
+  CH_KC_CG_FUSED_P = 10, /* ... pressure Poisson                                             */
+  CH_KC_CG_PX = 11,      /* deferred p / x update of the single-reduction CG                 */
+  CH_NKC = 12
 };
 
 /* Create a handle: allocates the rank's slab state and workspace on
@@ -150,6 +154,15 @@ int ch_comm_init(ch_handle* h, const void* id, size_t len);
 
 /* Rows owned by this handle: [*row0, *row0 + *nrows). */
 int ch_local_rows(const ch_handle* h, int32_t* row0, int32_t* nrows);
+
+/* Host-only (no device work, callable without a GPU): the 1-D slab
+ * decomposition in y that ch_create applies -- ny rows split over
+ * nranks * virtual_slabs slabs as evenly as possible, the first
+ * (ny mod total) slabs one row taller, each >= 2 rows; rank r owns slabs
+ * r*virtual_slabs .. (r+1)*virtual_slabs - 1.  Returns CH_ERR_ARG for an
+ * invalid decomposition (the same condition ch_create rejects). */
+int ch_partition(int32_t ny, int32_t nranks, int32_t rank, int32_t virtual_slabs, int32_t* row0,
+                 int32_t* nrows);
 
 /* Use `stream` (a cudaStream_t, may be NULL = legacy default) for all work. */
 int ch_set_stream(ch_handle* h, void* stream);

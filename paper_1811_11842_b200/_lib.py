@@ -19,7 +19,8 @@ FIELDS = {"phi": 0, "phi_prev": 1, "c": 2, "u": 3, "v": 4, "p": 5}
 SYSTEMS = ("ch", "nutrient", "u", "v", "p")
 OPS = {"ch": 0, "poisson": 1, "mom_u": 2, "mom_v": 3}
 SOLVERS = {"bicgstab": 0, "gmres": 1}
-KERNEL_CLASSES = ("cg_A", "cg_B", "cg_init", "ch_apply", "vec", "rhs", "gmres", "cg_fused")
+KERNEL_CLASSES = ("cg_A", "cg_B", "cg_init", "ch_apply", "vec", "rhs", "gmres", "cg_fused_c",
+                  "cg_fused_u", "cg_fused_v", "cg_fused_p", "cg_px")
 
 
 class Grid(C.Structure):
@@ -59,6 +60,8 @@ lib.ch_abi_version.restype = C.c_int
 lib.ch_comm_unique_id.argtypes = [_P, C.c_size_t]
 lib.ch_comm_init.argtypes = [_P, _P, C.c_size_t]
 lib.ch_local_rows.argtypes = [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+lib.ch_partition.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                             C.POINTER(C.c_int32)]
 lib.ch_set_stream.argtypes = [_P, _P]
 lib.ch_set_fields.argtypes = [_P, _P, _P, _P, _P, _P, C.c_int]
 lib.ch_set_field.argtypes = [_P, C.c_int, _P, C.c_int]
@@ -72,7 +75,7 @@ lib.ch_reset_stats.argtypes = [_P]
 lib.ch_enable_timing.argtypes = [_P, C.c_int]
 
 # every symbol the header declares (checked by tests/test_abi.py)
-EXPORTS = ("ch_create", "ch_comm_unique_id", "ch_comm_init", "ch_local_rows", "ch_set_stream",
+EXPORTS = ("ch_create", "ch_comm_unique_id", "ch_comm_init", "ch_local_rows", "ch_partition", "ch_set_stream",
            "ch_set_fields", "ch_set_field", "ch_step", "ch_get_fields", "ch_get_field",
            "ch_apply_operator", "ch_solve", "ch_get_stats", "ch_reset_stats", "ch_enable_timing",
            "ch_last_error", "ch_abi_version", "ch_destroy")

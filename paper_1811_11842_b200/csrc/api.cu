@@ -75,7 +75,7 @@ struct ch_handle {
   Comm* comm = nullptr;
   size_t arr_elems = 0;
   double* cgtab = nullptr;    // deferred-p/x CG coefficient tables, device [NSC][2][CGT]
-  int cg_defer = 8;           // block length m (2..12) of the deferred p/x CG (env CHB_DEFER)
+  int cg_defer = 16;          // block length m (2..32) of the deferred p/x CG (env CHB_DEFER)
   double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
   double* gm_host = nullptr;  // pinned mirror
   int vec = 3;                // CG: 3 single-reduction fused TMA sweep; two-kernel HS-CG with
@@ -402,7 +402,7 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   auto px = [&](long k_last, int n, int write_p) -> int {
     // z_k of iterations k_last - n + 1 .. k_last
     const long k0 = k_last - n + 1;
-    KTime kt(h, CH_KC_VEC, 8.0 * (n + 4) * cells);
+    KTime kt(h, CH_KC_CG_PX, 8.0 * (n + 4) * cells);
     for (int s = 0; s < h->S; ++s) {
       Slab& sl = h->sl[s];
       ZList zl;
@@ -440,7 +440,10 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
       const int first = (k == 0), dir = (k & 1) ? -1 : 1;
       const int zi = Zr[k % NZ], zo = Zr[(k + 1) % NZ], si = S[(k + 1) & 1], so = S[k & 1];
       {
-        KTime kt(h, CH_KC_CG_FUSED, cgs_bytes(kind, first) * cells, k + 1);
+        const int kc = sys == CH_SYS_U ? CH_KC_CG_FUSED_U
+                       : sys == CH_SYS_V ? CH_KC_CG_FUSED_V
+                       : sys == CH_SYS_P ? CH_KC_CG_FUSED_P : CH_KC_CG_FUSED;
+        KTime kt(h, kc, cgs_bytes(kind, first) * cells, k + 1);
         for (int s = 0; s < h->S; ++s) {
           Slab& sl = h->sl[s];
           launch_cgs_iter(opdesc(h, kind, sl), sl.g, sl.a[zi], sl.a[zo], sl.a[si], sl.a[so],
@@ -887,6 +890,21 @@ int gmres_solve(ch_handle* h, int sys, int xid, int bid) {
 extern "C" {
 
 int ch_abi_version(void) { return CH_ABI_VERSION; }
+
+// Host-only: the slab decomposition ch_create uses (balanced split of ny over
+// nranks * virtual_slabs slabs, the first ny % total one row taller).
+int ch_partition(int32_t ny, int32_t nranks, int32_t rank, int32_t virtual_slabs, int32_t* row0,
+                 int32_t* nrows) {
+  const int S = virtual_slabs < 1 ? 1 : virtual_slabs;
+  if (ny < 4 || nranks < 1 || rank < 0 || rank >= nranks || !row0 || !nrows) return CH_ERR_ARG;
+  const int total = nranks * S;
+  if (ny < 2 * total) return CH_ERR_ARG;
+  const int base = ny / total, rem = ny % total;
+  auto slab_row0 = [&](int k) { return k * base + std::min(k, rem); };
+  *row0 = slab_row0(rank * S);
+  *nrows = slab_row0(rank * S + S) - *row0;
+  return CH_OK;
+}
 
 const char* ch_last_error(const ch_handle* h) { return h ? h->err.c_str() : "null handle"; }
 

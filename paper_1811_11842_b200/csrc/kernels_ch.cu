@@ -13,11 +13,11 @@
 
 namespace chb {
 
-constexpr int CTX = 32, CTY = 8;
+constexpr int CTX = 32, CTY = 16;
 
+// periodic column (|overhang| <= 2 < nx)
 __device__ __forceinline__ int modc(int c, int nx) {
-  c %= nx;
-  return c < 0 ? c + nx : c;
+  return c < 0 ? c + nx : (c >= nx ? c - nx : c);
 }
 
 // Mirror-fold a global row and clamp to the stored range of the slab.

@@ -26,6 +26,16 @@ KEYS = [
 
 
 def kernel_class(name):
+    if "k_cgs_iter" in name:
+        m = re.search(r"k_cgs_iter<\(?(?:int\))?(\d+), \(?(?:int\))?(\d+), \(?(?:int\))?(\d+)", name)
+        if m:
+            bc, am, km = (int(v) for v in m.groups())
+            return {2: "cg_fused_v", 1: "cg_fused_u"}.get(bc, "cg_fused_c" if am else "cg_fused_p")
+        return "cg_fused"
+    if "k_cgs_px" in name:
+        return "cg_px"  # k_cgs_px
+    if "k_cgs_delta0" in name or "k_sum" in name:
+        return "cg_init"
     if "k_cg5_A" in name:
         return "cg_A"
     if "k_cg5_B" in name:
@@ -66,7 +76,7 @@ def rep_rows(path):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rep", action="append", default=[])
-    ap.add_argument("--launches")
+    ap.add_argument("--launches", action="append", default=[])
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     md = ["# ncu summary", ""]
@@ -88,8 +98,8 @@ def main():
                 traffic.setdefault(cls, {})
                 traffic[cls] = {"bytes": rb + wb, "kernel": d["name"][:120], "report": os.path.basename(rep)}
             md.append("")
-    if a.launches:
-        text = open(a.launches).read()
+    for lfile in a.launches:
+        text = open(lfile).read()
         start = text.find('"ID"')
         rows = list(csv.reader(io.StringIO(text[start:])))
         hdr = rows[0]
@@ -106,7 +116,7 @@ def main():
             tot[c] += v
             cnt[c] += 1
         T = sum(tot.values())
-        md.append(f"## launch list `{os.path.basename(a.launches)}` ({sum(cnt.values())} launches, "
+        md.append(f"## launch list `{os.path.basename(lfile)}` ({sum(cnt.values())} launches, "
                   f"`--metrics gpu__time_duration.sum --clock-control none`, serialised)")
         md.append("")
         md.append("| class | launches | total us | share | avg us |")
