@@ -9,3 +9,5 @@ timeout 300 python scripts/kbench.py --config 3 >> gpurun_out/kbench.jsonl 2>> g
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$? >> $S
 P="python scripts/kbench.py --solve poisson"
 timeout 300 $P > gpurun_out/plain_p.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cgs -s 6000 -c 17 -o gpurun_out/prof_cgs_p -f $P > gpurun_out/ncu_full_p.log 2>&1; echo ncufp=$? >> $S
+V="python scripts/kbench.py --solve mom_v"
+timeout 300 $V > gpurun_out/plain_v.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cgs_iter -s 3000 -c 2 -o gpurun_out/prof_cgs_v -f $V > gpurun_out/ncu_full_v.log 2>&1; echo ncufv=$? >> $S

@@ -77,6 +77,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rep", action="append", default=[])
     ap.add_argument("--launches", action="append", default=[])
+    ap.add_argument("--bench", help="bench.py JSON line: per-class event-timed step composition")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     md = ["# ncu summary", ""]
@@ -123,6 +124,24 @@ def main():
         md.append("|---|---|---|---|---|")
         for c in sorted(tot, key=lambda k: -tot[k]):
             md.append(f"| {c} | {cnt[c]} | {tot[c]:.0f} | {tot[c] / T:.3f} | {tot[c] / cnt[c]:.1f} |")
+        md.append("")
+    if a.bench:
+        line = json.loads(open(a.bench).read().strip().splitlines()[-1])
+        ks = line.get("kernels", {})
+        tot = sum(v["launches"] * v["avg_ms"] for v in ks.values())
+        md.append(f"## step composition of `{os.path.basename(a.bench)}` (CUDA events on the "
+                  f"library stream, every {line.get('steps')} timed steps, sampled launches)")
+        md.append("")
+        md.append("| class | launches/step | avg us | share | GB/s (algorithmic) |")
+        md.append("|---|---|---|---|---|")
+        steps = max(1, int(line.get("steps", 1)))
+        for k, v in sorted(ks.items(), key=lambda kv: -kv[1]["launches"] * kv[1]["avg_ms"]):
+            md.append(f"| {k} | {v['launches'] / steps:.0f} | {1e3 * v['avg_ms']:.1f} | "
+                      f"{v['launches'] * v['avg_ms'] / tot:.3f} | "
+                      f"{(v['GBps'] or 0):.0f} |")
+        md.append("")
+        md.append(f"value {line['value']:.4f} {line['unit']}, ms/step {line['ms_per_step']:.0f}, "
+                  f"roofline {json.dumps(line.get('roofline'))}")
         md.append("")
     with open(a.out + "_ncu_summary.md", "w") as f:
         f.write("\n".join(md) + "\n")
