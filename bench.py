@@ -203,13 +203,17 @@ def run_ours(args, rank, world, local_rank):
     dom = max(st["kernels"].items(), key=lambda kv: kv[1]["ms"] / max(kv[1]["timed"], 1) * kv[1]["launches"])
     name, kd = dom
     achieved = kd["bytes"] / (kd["ms"] / 1e3) / 1e9 if kd["ms"] > 0 else None
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as fh:
-            traffic = json.load(fh).get(name)
+            tr = json.load(fh).get(name)
+        if tr:   # dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full)
+            traffic = tr["bytes"]
+            traffic_src = tr["report"] + ": " + tr["kernel"][:60]
     roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "traffic_source": traffic_src,
             "peak_source": peak_kind,
             "bytes_per_launch": kd["bytes"] / max(kd["timed"], 1),
             "avg_launch_ms": kd["ms"] / max(kd["timed"], 1)}
