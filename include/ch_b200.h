@@ -138,7 +138,8 @@ enum {
   CH_KC_CG_FUSED_V = 9,  /* ... momentum v                                                   */
   CH_KC_CG_FUSED_P = 10, /* ... pressure Poisson                                             */
   CH_KC_CG_PX = 11,      /* deferred p / x update of the single-reduction CG                 */
-  CH_NKC = 12
+  CH_KC_OP_APPLY = 12,   /* isolated 5-point operator apply (ch_apply_operator)              */
+  CH_NKC = 13
 };
 
 /* Create a handle: allocates the rank's slab state and workspace on

@@ -20,7 +20,7 @@ SYSTEMS = ("ch", "nutrient", "u", "v", "p")
 OPS = {"ch": 0, "poisson": 1, "mom_u": 2, "mom_v": 3}
 SOLVERS = {"bicgstab": 0, "gmres": 1}
 KERNEL_CLASSES = ("cg_A", "cg_B", "cg_init", "ch_apply", "vec", "rhs", "gmres", "cg_fused_c",
-                  "cg_fused_u", "cg_fused_v", "cg_fused_p", "cg_px")
+                  "cg_fused_u", "cg_fused_v", "cg_fused_p", "cg_px", "op_apply")
 
 
 class Grid(C.Structure):

@@ -1150,8 +1150,10 @@ int ch_apply_operator(ch_handle* h, int op, const double* x, double* y, int wher
   int kind = 0;
   TRY(prep_operator(h, op, &kind));
   TRY(put(h, A_TMP, x, where));
+  const double cells = (double)h->grid.nx * (double)h->nrows / h->S;
   if (kind < 0) {
     TRY(halo(h, A_TMP, 2));
+    KTime kt(h, CH_KC_CH_APPLY, 24.0 * cells);   // read x, phi*; write y
     for (int s = 0; s < h->S; ++s) {
       Slab& sl = h->sl[s];
       launch_ch_apply(sl.g, chcoef(h, sl, false), sl.a[A_TMP], sl.a[A_B], 0, nullptr, nullptr, 0,
@@ -1159,11 +1161,14 @@ int ch_apply_operator(ch_handle* h, int op, const double* x, double* y, int wher
     }
   } else {
     TRY(halo(h, A_TMP, 1));
+    const double bpc = kind == OPK_POISSON_CONST ? 16.0 : 24.0;   // x, y (+ coefficient)
+    KTime kt(h, CH_KC_OP_APPLY, bpc * cells);
     for (auto& s : h->sl) launch_op5_apply(opdesc(h, kind, s), s.g, s.a[A_TMP], s.a[A_B], h->st);
   }
   TRY(check_launch(h, "apply_operator"));
   TRY(get(h, A_B, y, where));
-  if (where == CH_DEVICE) CK(cudaStreamSynchronize(h->st));
+  CK(cudaStreamSynchronize(h->st));
+  harvest(h, -1);
   return CH_OK;
 }
 

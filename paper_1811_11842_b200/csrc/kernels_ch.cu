@@ -8,8 +8,11 @@
 // w = Delta_h x^ on the halo-1 tile in shared memory, then the face-mobility
 // divergence -- one HBM read of x, dinv and phi* per cell, one write of y --
 // and fuses up to two dot products into the same pass.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "launch.h"
+#include "tma.cuh"
 
 namespace chb {
 
@@ -93,9 +96,224 @@ __global__ void __launch_bounds__(CTX* CTY)
   }
 }
 
+// --------------------------------------------------------------------------
+// Row-marching version (default): one CTA per (<= 256-column chunk x row
+// strip), x, D^-1 and phi* rows streamed into an 8-deep shared-memory ring by
+// 1-D bulk async copies (lane 0 of warps 0-2, one array each), two columns
+// per thread, x^ = D^-1 x and w = Delta_h x^ kept in three-row register
+// windows (w recomputed on the two neighbour columns each side instead of
+// exchanged), y = x^/dt + (G1/2) L_M w one row behind.  Same arithmetic as
+// k_ch_apply.  Per cell: read x, D^-1, phi* (+ dot operands), write y.
+namespace {
+constexpr int RM_T = 128;             // threads (4 warps)
+constexpr int RM_CW = 2 * RM_T;       // max columns per chunk
+constexpr int RM_SEG = RM_CW + 4;     // staged columns c0 - 2 .. c0 + wc + 1
+constexpr int RM_NST = 8;
+constexpr int RM_STAGE = 3 * RM_SEG;  // x | dinv | phi*
+
+__device__ __forceinline__ int rm_fold(const Geom& g, int gj) {
+  if (gj < 0) return -1 - gj;
+  if (gj >= g.ny) return 2 * g.ny - 1 - gj;
+  return gj;
+}
+
+__device__ __forceinline__ void rm_issue(const Geom& g, const double* base, uint32_t ring_s,
+                                         uint32_t bars_s, int slot, int gj, int c0, int wc,
+                                         int stream, bool use) {
+  const uint32_t bar = bars_s + 8u * (uint32_t)slot;
+  mbar_expect_tx_s(bar, use ? (uint32_t)(wc + 4) * 8u : 0u);
+  if (!use) return;
+  const double* row = base + (size_t)(rm_fold(g, gj) - g.j0 + GH) * g.pitch;
+  uint32_t d = ring_s + 8u * (uint32_t)(slot * RM_STAGE + stream * RM_SEG);
+  const int lo = c0 - 2, hi = c0 + wc + 2;
+  const int mlo = lo < 0 ? 0 : lo, mhi = hi > g.nx ? g.nx : hi;
+  if (lo < 0) {
+    bulk_g2s_s(d, row + (lo + g.nx), (uint32_t)(-lo) * 8u, bar);
+    d += (uint32_t)(-lo) * 8u;
+  }
+  bulk_g2s_s(d, row + mlo, (uint32_t)(mhi - mlo) * 8u, bar);
+  d += (uint32_t)(mhi - mlo) * 8u;
+  if (hi > g.nx) bulk_g2s_s(d, row, (uint32_t)(hi - g.nx) * 8u, bar);
+}
+
+__device__ __forceinline__ void rm_tile(int b, int nb, int ncb, int nyl, int& chunk, int& jl0,
+                                        int& jl1) {
+  const int q = nb / ncb, rem = nb % ncb;
+  int k, sc;
+  if (b < rem * (q + 1)) {
+    chunk = b / (q + 1);
+    k = b % (q + 1);
+    sc = q + 1;
+  } else {
+    const int bb = b - rem * (q + 1);
+    chunk = rem + bb / q;
+    k = bb % q;
+    sc = q;
+  }
+  jl0 = (int)(((long long)k * nyl) / sc);
+  jl1 = (int)(((long long)(k + 1) * nyl) / sc);
+}
+}  // namespace
+
+template <int NDOT, int PRE>
+__global__ void __launch_bounds__(RM_T) k_ch_rm(Geom g, ChCoef cc, const double* __restrict__ x,
+                                                double* __restrict__ y,
+                                                const double* __restrict__ d1,
+                                                const double* __restrict__ d2, int skip_done,
+                                                int skip_half, int ncb, int cw, RedArgs ra) {
+  if (skip_done && ra.sc->done) return;
+  if (skip_half && ra.sc->half) return;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bars[RM_NST];
+  const uint32_t ring_s = s_u32(smem), bars_s = s_u32(bars);
+  int chunk, jl0, jl1;
+  rm_tile(blockIdx.x, gridDim.x, ncb, g.nyl, chunk, jl0, jl1);
+  const int c0 = chunk * cw, wc = min(cw, g.nx - c0);
+  const int n = jl1 - jl0, nq = n + 4;  // ring rows j0+jl0-2 .. j0+jl1+1
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const bool own = 2 * t < wc;
+  const int ci = 2 * t + 2;  // staged index of the thread's first column
+  const int rbase = g.j0 + jl0 - 2;
+  const double* mysrc = warp == 0 ? x : (warp == 1 ? cc.dinv : cc.phis);
+  const bool myuse = warp == 0 || warp == 2 || (warp == 1 && PRE);
+  if (t == 0) {
+    for (int i = 0; i < RM_NST; ++i) mbar_init(bars + i, RM_T / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (lane == 0)
+    for (int q = 0; q < RM_NST && q < nq; ++q)
+      rm_issue(g, mysrc, ring_s, bars_s, q, rbase + q, c0, wc, warp, myuse);
+  auto slot = [&](int q) { return smem + (q % RM_NST) * RM_STAGE; };
+  auto xh = [&](const double* st, int idx) -> double {  // x^ = D^-1 x at staged index idx
+    const double v = st[idx];
+    return PRE ? v * st[RM_SEG + idx] : v;
+  };
+  auto wait_row = [&](int q) {
+    mbar_wait_s(bars_s + 8u * (uint32_t)(q % RM_NST), (uint32_t)((q / RM_NST) & 1));
+  };
+  // x^ rows (older -> newer) at columns c-1 .. c+2 of the thread's pair
+  double xa[4], xb[4], wm[4], wc_[4], wp[4];
+  wait_row(0);
+  wait_row(1);
+  for (int j = 0; j < 4; ++j) {
+    xa[j] = xh(slot(0), ci - 1 + j);
+    xb[j] = xh(slot(1), ci - 1 + j);
+    wm[j] = wc_[j] = 0.0;
+  }
+  const double L = cc.Lambda, idt = 1.0 / cc.dt;
+  double s0 = 0.0, s1 = 0.0;
+  for (int k = 0; k <= n + 1; ++k) {
+    wait_row(k + 2);
+    // w on ring row k + 1 (x^ rows k, k+1, k+2) at columns c-1 .. c+2
+    const double* sc1 = slot(k + 1);
+    const double* sc2 = slot(k + 2);
+    double xn[4];
+    for (int j = 0; j < 4; ++j) xn[j] = xh(sc2, ci - 1 + j);
+    const double xl = xh(sc1, ci - 2), xr = xh(sc1, ci + 3);
+    for (int j = 0; j < 4; ++j) {
+      const double xw = j == 0 ? xl : xb[j - 1], xe = j == 3 ? xr : xb[j + 1];
+      wp[j] = (xe - 2.0 * xb[j] + xw) * g.ihx2 + (xn[j] - 2.0 * xb[j] + xa[j]) * g.ihy2;
+    }
+    // y on ring row k (owned rows 2 .. n+1): w rows k-1 (wm), k (wc_), k+1 (wp)
+    if (k >= 2 && own) {
+      const int gj = rbase + k;
+      const double* ps0 = slot(k - 1) + 2 * RM_SEG;
+      const double* ps1 = slot(k) + 2 * RM_SEG;
+      const double* ps2 = slot(k + 1) + 2 * RM_SEG;
+      double yv[2];
+      for (int j = 0; j < 2; ++j) {
+        const int cc_ = ci + j;      // staged index of this column
+        const double pc = ps1[cc_];
+        const double mE = L * fmax(0.0, 0.5 * (pc + ps1[cc_ + 1]));
+        const double mW = L * fmax(0.0, 0.5 * (pc + ps1[cc_ - 1]));
+        const double mN = (gj == g.ny - 1) ? 0.0 : L * fmax(0.0, 0.5 * (pc + ps2[cc_]));
+        const double mS = (gj == 0) ? 0.0 : L * fmax(0.0, 0.5 * (pc + ps0[cc_]));
+        const double w0 = wc_[j + 1];
+        const double div = (mE * (wc_[j + 2] - w0) - mW * (w0 - wc_[j])) * g.ihx2 +
+                           (mN * (wp[j + 1] - w0) - mS * (w0 - wm[j + 1])) * g.ihy2;
+        yv[j] = xa[j + 1] / cc.dt + cc.g1h * div;
+      }
+      (void)idt;
+      const size_t o = off(g, gj, c0 + 2 * t);
+      *reinterpret_cast<double2*>(y + o) = make_double2(yv[0], yv[1]);
+      if (NDOT >= 1) {
+        const double2 a = *reinterpret_cast<const double2*>(d1 + o);
+        s0 += yv[0] * a.x + yv[1] * a.y;
+      }
+      if (NDOT >= 2) {
+        if (d2) {
+          const double2 b = *reinterpret_cast<const double2*>(d2 + o);
+          s1 += yv[0] * b.x + yv[1] * b.y;
+        } else {
+          s1 += yv[0] * yv[0] + yv[1] * yv[1];
+        }
+      }
+    }
+    __syncthreads();  // ring row k - 1 consumed by every warp
+    if (lane == 0 && k >= 1 && k - 1 + RM_NST < nq) {
+      fence_proxy_async();
+      rm_issue(g, mysrc, ring_s, bars_s, (k - 1) % RM_NST, rbase + k - 1 + RM_NST, c0, wc, warp,
+               myuse);
+    }
+    for (int j = 0; j < 4; ++j) {
+      xa[j] = xb[j];
+      xb[j] = xn[j];
+      wm[j] = wc_[j];
+      wc_[j] = wp[j];
+    }
+  }
+  if (NDOT == 1) {
+    double v[1] = {s0};
+    block_reduce_finalize<1>(v, ra);
+  } else if (NDOT == 2) {
+    double v[2] = {s0, s1};
+    block_reduce_finalize<2>(v, ra);
+  }
+}
+
+namespace {
+template <int NDOT, int PRE>
+void launch_rm(const Geom& g, const ChCoef& cc, const double* x, double* y, const double* d1,
+               const double* d2, int skip_done, int skip_half, const RedArgs& ra,
+               cudaStream_t st) {
+  auto kern = k_ch_rm<NDOT, PRE>;
+  constexpr size_t smem = (size_t)RM_NST * RM_STAGE * sizeof(double);
+  static int per_sm = -1;
+  static int nsm = 0;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RM_T, smem);
+    if (per_sm < 1) per_sm = 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int ncb = (g.nx + RM_CW - 1) / RM_CW;
+  int cw = (g.nx + ncb - 1) / ncb;
+  cw += cw & 1;
+  long nb = (long)nsm * per_sm;
+  if (nb < ncb) nb = ncb;
+  if (nb > (long)ncb * g.nyl) nb = (long)ncb * g.nyl;
+  kern<<<(unsigned)nb, RM_T, smem, st>>>(g, cc, x, y, d1, d2, skip_done, skip_half, ncb, cw, ra);
+}
+}  // namespace
+
 void launch_ch_apply(const Geom& g, const ChCoef& cc, const double* x, double* y, int ndot,
                      const double* d1, const double* d2, int skip_if_done, int skip_if_half,
                      const RedArgs& ra, cudaStream_t st) {
+  if ((g.nx % 2) == 0 && !getenv("CHB_CH_TILE")) {  // row-marching kernel (even nx)
+    if (cc.dinv) {
+      if (ndot == 0) launch_rm<0, 1>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
+      else if (ndot == 1) launch_rm<1, 1>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
+      else launch_rm<2, 1>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
+    } else {
+      if (ndot == 0) launch_rm<0, 0>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
+      else if (ndot == 1) launch_rm<1, 0>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
+      else launch_rm<2, 0>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
+    }
+    return;
+  }
   dim3 grid((g.nx + CTX - 1) / CTX, (g.nyl + CTY - 1) / CTY);
   dim3 block(CTX, CTY);
   if (ndot == 0)
