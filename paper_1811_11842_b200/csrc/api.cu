@@ -30,7 +30,7 @@ enum Arr {
   A_N = A_ZH0 + CGM - 1
 };
 
-constexpr int MAX_BLOCKS = 1 << 17;
+constexpr int MAX_BLOCKS = 1 << 20;  // reduction partials (8 doubles each): covers 16384^2 grids
 constexpr int NSC = CH_NSYS + 2;  // one KScal per system + apply + spare
 
 struct Slab {

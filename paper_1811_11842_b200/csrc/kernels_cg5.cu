@@ -689,9 +689,18 @@ void launch_op5_apply(const OpDesc& d, const Geom& g, const double* x, double* y
                                                                                    strip)));
 }
 
-static dim3 grid_pw(const Geom& g) {
-  int gy = g.nyl < 4096 ? g.nyl : 4096;
-  return dim3((g.nx + 255) / 256, gy);
+static dim3 grid_pw(const Geom& g) {  // ~8 CTAs per SM (bounded reduction partials)
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int gx = (g.nx + 255) / 256;
+  int gy = (nsm * 8 + gx - 1) / gx;
+  if (gy > g.nyl) gy = g.nyl;
+  if (gy < 1) gy = 1;
+  return dim3(gx, gy);
 }
 
 void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace, int odd_only,

@@ -331,9 +331,20 @@ void launch_ch_apply(const Geom& g, const ChCoef& cc, const double* x, double* y
   for (int jl = blockIdx.y; jl < (g).nyl; jl += gridDim.y)          \
     if (c_ < (g).nx)
 
+// ~8 CTAs per SM: enough bytes in flight, and few enough partial sums that the
+// last CTA's fixed-order reduction stays short
 static dim3 grid_pw(const Geom& g) {
-  int gy = g.nyl < 2048 ? g.nyl : 2048;
-  return dim3((g.nx + 255) / 256, gy);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int gx = (g.nx + 255) / 256;
+  int gy = (nsm * 8 + gx - 1) / gx;
+  if (gy > g.nyl) gy = g.nyl;
+  if (gy < 1) gy = 1;
+  return dim3(gx, gy);
 }
 
 __global__ void __launch_bounds__(256) k_bi_init(Geom g, const double* __restrict__ y,

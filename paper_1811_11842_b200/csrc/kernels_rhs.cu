@@ -189,16 +189,19 @@ __global__ void __launch_bounds__(256) k_mom_rhs_v(Geom g, Phys ph, StateP s,
 __global__ void __launch_bounds__(256) k_div(Geom g, const double* __restrict__ us,
                                              const double* __restrict__ vs, double* b,
                                              RedArgs ra) {
+  // grid-strided over rows: the number of CTAs (= reduction partials) stays bounded
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int jl = blockIdx.y * blockDim.y + threadIdx.y;
   double acc = 0.0;
-  if (i < g.nx && jl < g.nyl) {
-    const int j = g.j0 + jl;
+  if (i < g.nx) {
     const int ie = wrapc(i + 1, g.nx);
-    const double d = (us[off(g, j, ie)] - us[off(g, j, i)]) * g.ihx +
-                     (ldf<BC_VFACE>(vs, g, j + 1, i) - ldf<BC_VFACE>(vs, g, j, i)) * g.ihy;
-    b[off(g, j, i)] = d;
-    acc = d;
+    for (int jl = blockIdx.y * blockDim.y + threadIdx.y; jl < g.nyl;
+         jl += gridDim.y * blockDim.y) {
+      const int j = g.j0 + jl;
+      const double d = (us[off(g, j, ie)] - us[off(g, j, i)]) * g.ihx +
+                       (ldf<BC_VFACE>(vs, g, j + 1, i) - ldf<BC_VFACE>(vs, g, j, i)) * g.ihy;
+      b[off(g, j, i)] = d;
+      acc += d;
+    }
   }
   double v[1] = {acc};
   block_reduce_finalize<1>(v, ra);
@@ -243,7 +246,9 @@ void launch_mom_rhs_v(const Geom& g, const Phys& ph, StateP s, const double* phi
 }
 void launch_div(const Geom& g, const double* us, const double* vs, double* b, const RedArgs& ra,
                 cudaStream_t st) {
-  k_div<<<grid2(g), blk2, 0, st>>>(g, us, vs, b, ra);
+  dim3 gr = grid2(g);
+  if (gr.y > 256) gr.y = 256;   // <= 512 x 256 partials even at 16384^2
+  k_div<<<gr, blk2, 0, st>>>(g, us, vs, b, ra);
 }
 void launch_project(const Geom& g, const Phys& ph, const double* phi1, const double* us,
                     const double* vs, const double* p, double* u, double* v, cudaStream_t st) {

@@ -71,3 +71,11 @@ __device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 }  // namespace chb
+
+namespace chb {
+// Bulk prefetch of a global range into L2 (no shared memory, no completion
+// tracking): lets a shallow shared-memory ring run far ahead of HBM latency.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+}  // namespace chb
