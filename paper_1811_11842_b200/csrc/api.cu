@@ -75,7 +75,8 @@ struct ch_handle {
   Comm* comm = nullptr;
   size_t arr_elems = 0;
   double* cgtab = nullptr;    // deferred-p/x CG coefficient tables, device [NSC][2][CGT]
-  int cg_defer = 16;          // block length m (2..32) of the deferred p/x CG (env CHB_DEFER)
+  int cg_defer = 32;          // block length m (2..32) of the deferred p/x CG (env CHB_DEFER);
+                              // reduced at ch_create if the z history would not fit
   double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
   double* gm_host = nullptr;  // pinned mirror
   int vec = 3;                // CG: 3 single-reduction fused TMA sweep; two-kernel HS-CG with
@@ -977,6 +978,17 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
     maxrows = std::max(maxrows, slab_row0(k + 1) - slab_row0(k));
   }
   h->arr_elems = (size_t)(maxrows + 2 * GH) * pitch;
+  {
+    // the z history (m - 1 arrays beyond the fixed set) may use at most ~half of
+    // the device memory left after the fixed arrays
+    size_t freeb = 0, totb = 0;
+    if (cudaMemGetInfo(&freeb, &totb) == cudaSuccess) {
+      const double arr = (double)h->arr_elems * sizeof(double) * S;
+      const double fixed = arr * A_ZH0;
+      while (h->cg_defer > 2 && fixed + arr * (h->cg_defer - 1) > 0.8 * (double)freeb)
+        h->cg_defer /= 2;
+    }
+  }
   h->sl.resize(S);
   for (int s = 0; s < S; ++s) {
     Slab& sl = h->sl[s];
