@@ -485,3 +485,25 @@ def test_isolated_solve_deferred_modes(defer, op, monkeypatch):
     x, ref, it_gpu, it_ref = _solve_case(128, 96, op, rtol=1e-12, rho_n=0.7)
     assert _rel(x, ref) <= 1e-9, (op, _rel(x, ref))
     assert abs(it_gpu - it_ref) <= 2, (it_gpu, it_ref)
+
+
+@pytest.mark.parametrize("nx,ny", [(64, 48), (300, 70), (520, 33)])
+def test_persistent_cg_matches_oracle(nx, ny, monkeypatch):
+    """Whole CG solves as one cooperative launch (grid barrier + last-CTA
+    finalize per iteration, in-kernel p/x blocks): same fields and iteration
+    counts as the oracle."""
+    monkeypatch.setenv("CHB_PERSIST", "1")
+    got, ref, st, iters = _run_both(nx, ny, 1, rtol=1e-12)
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
+    for sysname in ("nutrient", "u", "v", "p"):
+        assert abs(st["iters_last"][sysname] - iters[-1][sysname]) <= 2, (sysname, st, iters)
+
+
+@pytest.mark.parametrize("op", ["poisson", "mom_v"])
+def test_persistent_isolated_solve(op, monkeypatch):
+    monkeypatch.setenv("CHB_PERSIST", "1")
+    monkeypatch.setenv("CHB_DEFER", "5")
+    x, ref, it_gpu, it_ref = _solve_case(128, 96, op, rtol=1e-12, rho_n=0.7)
+    assert _rel(x, ref) <= 1e-9, (op, _rel(x, ref))
+    assert abs(it_gpu - it_ref) <= 2, (it_gpu, it_ref)
