@@ -223,6 +223,49 @@ int fin_slabs(ch_handle* h, int fin, int sys, int K) {
   return check_launch(h, "finalize_slabs");
 }
 
+// Exchange `w` ghost rows of array `id` between the slabs of this process.
+int halo_local(ch_handle* h, int id, int w) {
+  for (int s = 0; s + 1 < h->S; ++s) {
+    Slab& lo = h->sl[s];
+    Slab& hi = h->sl[s + 1];
+    const size_t pitch = lo.g.pitch;
+    double* src = lo.a[id] + (size_t)(lo.g.nyl + GH - w) * pitch;
+    double* dst = hi.a[id] + (size_t)(GH - w) * pitch;
+    CK(cudaMemcpyAsync(dst, src, w * pitch * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    src = hi.a[id] + (size_t)GH * pitch;
+    dst = lo.a[id] + (size_t)(lo.g.nyl + GH) * pitch;
+    CK(cudaMemcpyAsync(dst, src, w * pitch * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+  }
+  return CH_OK;
+}
+
+// One CG iteration's communication: partial-sum combination (finalize) and
+// the ghost rows of z' (2) and s (1).  Across processes the allgather and the
+// halo rows go in ONE NCCL group.
+int iter_exchange(ch_handle* h, int fin, int sys, int K, int zid, int sid) {
+  if (h->nslabs_total == 1) return CH_OK;
+  if (!h->comm) {
+    TRY(fin_slabs(h, fin, sys, K));
+    TRY(halo_local(h, zid, 2));
+    return halo_local(h, sid, 1);
+  }
+  TRY(halo_local(h, zid, 2));
+  TRY(halo_local(h, sid, 1));
+  const Slab& first = h->sl.front();
+  const Slab& last = h->sl.back();
+  HaloSpec hs[2] = {{first.a[zid], last.a[zid], last.g.nyl, 2},
+                    {first.a[sid], last.a[sid], last.g.nyl, 1}};
+  if (comm_iter_exchange(h->comm, h->tot_local, h->tot, (size_t)h->S * 8, hs, 2,
+                         first.g.pitch, h->st) != 0) {
+    h->err = "comm iteration exchange failed";
+    return CH_ERR_COMM;
+  }
+  RedArgs ra = rargs(h, fin, sys, 0);
+  launch_finalize_slabs(h->tot, h->nslabs_total, K, ra, h->st);
+  h->stats.launches += 1;
+  return check_launch(h, "finalize_slabs");
+}
+
 // Exchange `w` ghost rows of array `id` between neighbouring slabs.
 int halo(ch_handle* h, int id, int w) {
   if (h->nslabs_total == 1) return CH_OK;
@@ -494,9 +537,7 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
                           first, dir, rargs(h, FIN_CGS, sys, s), h->st);
         }
       }
-      TRY(fin_slabs(h, FIN_CGS, sys, 3));
-      TRY(halo(h, zo, 2));
-      TRY(halo(h, so, 1));
+      TRY(iter_exchange(h, FIN_CGS, sys, 3, zo, so));
       if ((k + 1) % m == 0) TRY(px(k, m, 1));
     }
     TRY(check_launch(h, "cgs iteration"));

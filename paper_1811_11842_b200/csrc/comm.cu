@@ -116,6 +116,33 @@ int comm_halo(Comm* c, double* first_base, int first_nyl, double* last_base, int
   return a.GroupEnd() == ncclSuccess ? 0 : 1;
 }
 
+int comm_iter_exchange(Comm* c, const double* send, double* recv, size_t count,
+                       const HaloSpec* halos, int nhalo, int pitch, cudaStream_t st) {
+  NcclApi& a = api();
+  const int GH = chb::GH;
+  if (a.GroupStart() != ncclSuccess) return 1;
+  int bad = 0;
+  if (count) bad |= a.AllGather(send, recv, count, ncclFloat64, c->comm, st) != ncclSuccess;
+  for (int k = 0; k < nhalo; ++k) {
+    const HaloSpec& h = halos[k];
+    const size_t n = (size_t)h.w * pitch;
+    if (c->rank > 0) {
+      bad |= a.Send(h.first_base + (size_t)GH * pitch, n, ncclFloat64, c->rank - 1, c->comm, st) !=
+             ncclSuccess;
+      bad |= a.Recv(h.first_base + (size_t)(GH - h.w) * pitch, n, ncclFloat64, c->rank - 1,
+                    c->comm, st) != ncclSuccess;
+    }
+    if (c->rank + 1 < c->nranks) {
+      bad |= a.Send(h.last_base + (size_t)(h.last_nyl + GH - h.w) * pitch, n, ncclFloat64,
+                    c->rank + 1, c->comm, st) != ncclSuccess;
+      bad |= a.Recv(h.last_base + (size_t)(h.last_nyl + GH) * pitch, n, ncclFloat64, c->rank + 1,
+                    c->comm, st) != ncclSuccess;
+    }
+  }
+  bad |= a.GroupEnd() != ncclSuccess;
+  return bad ? 1 : 0;
+}
+
 double comm_allreduce_host(Comm* c, double v) {
   cudaMemcpy(c->scratch, &v, sizeof v, cudaMemcpyHostToDevice);
   api().AllReduce(c->scratch, c->scratch + 1, 1, ncclFloat64, ncclSum, c->comm, 0);

@@ -18,5 +18,16 @@ int comm_allgather(Comm* c, const double* send, double* recv, size_t count, cuda
 // the last local slab its top w rows with rank+1 (non-periodic in y).
 int comm_halo(Comm* c, double* first_base, int first_nyl, double* last_base, int last_nyl,
               int pitch, int w, cudaStream_t st);
+// One NCCL group per CG iteration: the allgather of the per-slab partial sums
+// and the halo rows of up to 4 arrays (first/last local slab bases, width w[k])
+// travel together, so an iteration costs one NCCL launch instead of three.
+struct HaloSpec {
+  double* first_base;
+  double* last_base;
+  int last_nyl;
+  int w;
+};
+int comm_iter_exchange(Comm* c, const double* send, double* recv, size_t count,
+                       const HaloSpec* halos, int nhalo, int pitch, cudaStream_t st);
 double comm_allreduce_host(Comm* c, double v);
 void comm_destroy(Comm* c);

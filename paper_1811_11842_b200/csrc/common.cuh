@@ -289,16 +289,27 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
     }
   }
   __syncthreads();
-  if (!am_last || wid != 0) return;
+  if (!am_last) return;
   __threadfence();
+  // the last CTA sums the partials with all its warps (fixed partition and
+  // order: deterministic), then one thread finalizes
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double t = 0.0;
+    for (int b = wid * 32 + lane; b < nb; b += nw * 32) t += __ldcg(ra.part + (size_t)b * 8 + k);
+    t = warp_sum(t);
+    if (lane == 0) sm[wid][k] = t;
+  }
+  __syncthreads();
+  if (tid != 0) return;
   double res[K > 0 ? K : 1];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     double t = 0.0;
-    for (int b = lane; b < nb; b += 32) t += __ldcg(ra.part + (size_t)b * 8 + k);
-    res[k] = warp_sum(t);
+    for (int w = 0; w < nw; ++w) t += sm[w][k];
+    res[k] = t;
   }
-  if (lane == 0) {
+  {
     *ra.ticket = 0u;
     if (ra.inline_fin) {
       finalize(ra.fin, res, ra.sc, ra.fc);

@@ -42,7 +42,7 @@ def kernel_class(name):
         return "cg_B"
     if "k_cg5_init" in name:
         return "cg_init"
-    if "k_ch_apply" in name:
+    if "k_ch_apply" in name or "k_ch_rm" in name:
         return "ch_apply"
     if re.search(r"k_(bi|gm|sub_mean|cg5_finish)", name):
         return "vec"

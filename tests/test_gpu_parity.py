@@ -507,3 +507,30 @@ def test_persistent_isolated_solve(op, monkeypatch):
     x, ref, it_gpu, it_ref = _solve_case(128, 96, op, rtol=1e-12, rho_n=0.7)
     assert _rel(x, ref) <= 1e-9, (op, _rel(x, ref))
     assert abs(it_gpu - it_ref) <= 2, (it_gpu, it_ref)
+
+
+def test_config2_1024_steps_invariants():
+    """BASELINE.json configs[2] (1024^2, here 5 of its 50 steps): every solve
+    reaches rtol, the projected velocity is divergence free to the pressure
+    solve's accuracy, and with growth off phi's mass is conserved."""
+    from paper_1811_11842_b200 import Simulation
+    from oracle import explicit as ex
+    from workloads import initial_fields
+    n = 1024
+    f = initial_fields(n, n, seed=0)
+    sim = Simulation(n, n, eps=0.0)
+    sim.set_fields(**f)
+    m0 = ex.mass(f["phi"])
+    for _ in range(5):
+        sim.step(1)
+        st = sim.stats()
+        for k, r in st["resid_last"].items():
+            assert r <= 1e-10, (k, r)
+    g = sim.get_fields(("phi", "u", "v", "p"))
+    ap = sim.apply_operator("poisson", g["p"])
+    sim.close()
+    assert abs(ex.mass(g["phi"]) - m0) / m0 < 1e-11
+    d = ex.divergence(g["u"], g["v"])
+    rhs = d + ap
+    rhs -= rhs.mean()
+    assert np.linalg.norm(d - d.mean()) <= 1e-8 * np.linalg.norm(rhs)
