@@ -1,6 +1,8 @@
-# one gpurun call: wave-count experiment, tests
+# one gpurun call: tests, solve timing, bench
 mkdir -p gpurun_out
 S=gpurun_out/status.txt; : > $S
 rm -f gpurun_out/kbench.jsonl gpurun_out/*.ncu-rep
-for w in 1 2 3 4; do for op in poisson mom_v; do CHB_WAVES=$w timeout 300 python scripts/kbench.py --solve $op | sed "s/^{/{\"waves\": $w, /" >> gpurun_out/kbench.jsonl 2>> gpurun_out/kbench.err; done; done
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$? >> $S
 timeout 1500 python -m pytest tests -m gpu -q --durations=25 > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> $S
+for op in poisson mom_v; do timeout 300 python scripts/kbench.py --solve $op >> gpurun_out/kbench.jsonl 2>> gpurun_out/kbench.err; done
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$? >> $S
