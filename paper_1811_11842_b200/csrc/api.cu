@@ -77,6 +77,11 @@ struct ch_handle {
   double* cgtab = nullptr;    // deferred-p/x CG coefficient tables, device [NSC][2][CGT]
   unsigned int* pbar = nullptr; // persistent-CG grid barrier: count, generation, abort flag
   int persist = 0;            // single-slab CG solves as one cooperative launch (env CHB_PERSIST)
+  int px_async = 0;           // p/x updates on a side stream, overlapped with the sweeps
+                              // (block length m/2, z ring 2m/2+1; env CHB_PXASYNC)
+  int cur_m = 0;              // block length of the solve in flight (0: cg_defer)
+  cudaStream_t st2 = nullptr; // side stream of the asynchronous p/x updates
+  cudaEvent_t pxev[5] = {};   // [0..3] p/x done per block (mod 4), [4] sweep-side marker
   int cg_defer = 32;          // block length m (2..32) of the deferred p/x CG (env CHB_DEFER);
                               // reduced at ch_create if the z history would not fit
   double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
@@ -197,7 +202,7 @@ RedArgs rargs(ch_handle* h, int fin, int sys, int slab) {
   ra.fc.rtol2 = h->prm.rtol * h->prm.rtol;
   ra.fc.ncells = (double)h->grid.nx * (double)h->grid.ny;
   ra.fc.tab = h->cgtab ? h->cgtab + (size_t)sys * 2 * CGT : nullptr;
-  ra.fc.m = h->cg_defer;
+  ra.fc.m = h->cur_m > 0 ? h->cur_m : h->cg_defer;
   ra.fc.pad = 0;
   ra.fin = fin;
   ra.inline_fin = (h->nslabs_total == 1);
@@ -435,9 +440,16 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   if (wid >= 0) TRY(halo(h, wid, 2));
   if (AM) TRY(halo(h, A_CA, 1));
   TRY(halo(h, xid, 1));
-  // z ring of m + 1 buffers (p/x deferred over blocks of m sweeps)
-  const int m = h->cg_defer;
-  const int NZ = m + 1;
+  // z ring of m + 1 buffers (p/x deferred over blocks of m sweeps); with the
+  // asynchronous p/x the same buffers hold 2 m' + 1 z's of blocks m' = m / 2
+  const bool apx = h->px_async && !h->persist && h->cg_defer >= 4;
+  const int m = apx ? h->cg_defer / 2 : h->cg_defer;
+  const int NZ = apx ? 2 * m + 1 : m + 1;
+  h->cur_m = m;
+  if (apx && !h->st2) {
+    CK(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+    for (auto& e : h->pxev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   int Zr[CGM + 1];
   Zr[0] = A_Z;
   Zr[1] = A_R;
@@ -448,6 +460,25 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   auto px = [&](long k_last, int n, int write_p) -> int {
     // z_k of iterations k_last - n + 1 .. k_last
     const long k0 = k_last - n + 1;
+    if (apx && write_p) {
+      // side stream: starts when the block's last sweep is done; the main stream
+      // waits for it only m' - 1 sweeps later (before the finalize that reuses
+      // its coefficient table, and before its z's are overwritten)
+      const long b = k_last / m;
+      CK(cudaEventRecord(h->pxev[4], h->st));
+      CK(cudaStreamWaitEvent(h->st2, h->pxev[4], 0));
+      for (int s = 0; s < h->S; ++s) {
+        Slab& sl = h->sl[s];
+        ZList zl;
+        for (int j = 0; j < CGM; ++j) zl.z[j] = j < n ? sl.a[Zr[(k0 + j) % NZ]] : nullptr;
+        launch_cgs_px(sl.g, zl, n, k0 == 0, write_p, (int)(k_last + 1),
+                      tab + ((k_last / m) & 1) * CGT, h->sc + sys, sl.a[P], sl.a[xid], h->st2);
+      }
+      h->stats.launches += h->S;
+      h->stats.kc_launches[CH_KC_CG_PX] += h->S;
+      CK(cudaEventRecord(h->pxev[b & 3], h->st2));
+      return check_launch(h, "cgs_px async");
+    }
     KTime kt(h, CH_KC_CG_PX, 8.0 * (n + 4) * cells);
     for (int s = 0; s < h->S; ++s) {
       Slab& sl = h->sl[s];
@@ -528,6 +559,8 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   for (;;) {
     for (int it = 0; it < chunk; ++it, ++k) {
       const int first = (k == 0), dir = (k & 1) ? -1 : 1;
+      if (apx && (k + 1) % m == 0 && k + 1 >= 2 * m)  // block (k+1)/m - 2's p/x must be done
+        CK(cudaStreamWaitEvent(h->st, h->pxev[((k + 1) / m - 2) & 3], 0));
       const int zi = Zr[k % NZ], zo = Zr[(k + 1) % NZ], si = S[(k + 1) & 1], so = S[k & 1];
       {
         KTime kt(h, kc_sys, cgs_bytes(kind, first) * cells, k + 1);
@@ -547,6 +580,10 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   }
   }
   const long K = h->sch[sys].iter;
+  if (apx) {  // every asynchronous p/x launched so far is done before the tail
+    CK(cudaEventRecord(h->pxev[4], h->st2));
+    CK(cudaStreamWaitEvent(h->st, h->pxev[4], 0));
+  }
   if (K > 0 && K % m != 0) TRY(px(K - 1, (int)(K % m), 0));
   {
     KTime kt(h, CH_KC_VEC, 24.0 * cells);
@@ -1010,6 +1047,9 @@ static void destroy_mem(ch_handle* h) {
   if (h->gm_dev) cudaFree(h->gm_dev);
   if (h->cgtab) cudaFree(h->cgtab);
   if (h->pbar) cudaFree(h->pbar);
+  for (auto& e : h->pxev)
+    if (e) cudaEventDestroy(e);
+  if (h->st2) cudaStreamDestroy(h->st2);
   if (h->gm_host) cudaFreeHost(h->gm_host);
   for (auto& r : h->tm.pending) {
     cudaEventDestroy(r.e0);
@@ -1052,6 +1092,7 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   if (const char* e = getenv("CHB_PDL")) h->pdl = atoi(e) != 0;
   if (const char* e = getenv("CHB_DEFER")) h->cg_defer = std::min(std::max(2, atoi(e)), CGM);
   if (const char* e = getenv("CHB_PERSIST")) h->persist = atoi(e) != 0;
+  if (const char* e = getenv("CHB_PXASYNC")) h->px_async = atoi(e) != 0;
   memset(&h->stats, 0, sizeof(ch_stats));
   // rows: balanced split of ny over `total` slabs (first ny % total get one more)
   const int base = G.ny / total, rem = G.ny % total;

@@ -36,6 +36,13 @@ if a.solve:
     if a.solve == "mom_v":
         b[0] = 0.0
     sim.solve(a.solve, b)          # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sim.solve(a.solve, b)          # untimed per kernel: the solve's own wall time
+    e1.record()
+    torch.cuda.synchronize()
+    solve_ms = e0.elapsed_time(e1)
     sim.reset_stats()
     sim.enable_timing(a.stride)
     sim.solve(a.solve, b)
@@ -45,8 +52,10 @@ else:
     sim.enable_timing(a.stride)
     sim.step(a.steps)
 st = sim.stats()
-out = {"variant": os.environ.get("CHB_VEC", "default"), "defer": os.environ.get("CHB_DEFER", "8"),
+out = {"variant": os.environ.get("CHB_VEC", "default"), "defer": os.environ.get("CHB_DEFER", "32"),
        "solve": a.solve, "config": cfg["name"], "iters": st["iters_last"], "kernels": {}}
+if a.solve:
+    out["solve_ms"] = solve_ms
 for k, v in st["kernels"].items():
     if v["timed"]:
         out["kernels"][k] = {"launches": v["launches"], "avg_us": 1e3 * v["ms"] / v["timed"],

@@ -534,3 +534,18 @@ def test_config2_1024_steps_invariants():
     rhs = d + ap
     rhs -= rhs.mean()
     assert np.linalg.norm(d - d.mean()) <= 1e-8 * np.linalg.norm(rhs)
+
+
+@pytest.mark.parametrize("defer", ["4", "8", "32"])
+@pytest.mark.parametrize("nx,ny", [(64, 48), (300, 70)])
+def test_async_px_matches_oracle(defer, nx, ny, monkeypatch):
+    """p/x block updates on a side stream overlapped with the sweeps (the main
+    stream waits for block b before the finalize that reuses its coefficient
+    table): same fields and iteration counts as the oracle."""
+    monkeypatch.setenv("CHB_PXASYNC", "1")
+    monkeypatch.setenv("CHB_DEFER", defer)
+    got, ref, st, iters = _run_both(nx, ny, 1, rtol=1e-12)
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (defer, k, _rel(got[k], ref[k]))
+    for sysname in ("nutrient", "u", "v", "p"):
+        assert abs(st["iters_last"][sysname] - iters[-1][sysname]) <= 2, (sysname, st, iters)
