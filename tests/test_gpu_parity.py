@@ -549,3 +549,12 @@ def test_async_px_matches_oracle(defer, nx, ny, monkeypatch):
         assert _rel(got[k], ref[k]) <= 1e-9, (defer, k, _rel(got[k], ref[k]))
     for sysname in ("nutrient", "u", "v", "p"):
         assert abs(st["iters_last"][sysname] - iters[-1][sysname]) <= 2, (sysname, st, iters)
+
+
+@pytest.mark.parametrize("nx,ny", [(45, 38), (33, 21), (8, 6), (6, 4), (4, 4)])
+def test_odd_and_tiny_grids_match_oracle(nx, ny):
+    """Odd nx (two-kernel CG and tile CH apply fallback) and the smallest grids
+    the library accepts (single chunk, strips of one or two rows)."""
+    got, ref, st, iters = _run_both(nx, ny, 1, rtol=1e-12, Lambda=1e-5)
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (nx, ny, k, _rel(got[k], ref[k]))
