@@ -1,7 +1,6 @@
-# asynchronous p/x: parity + timing
+# per-rank slab shapes of the strong-scaling runs (4096 x 4096/N), isolated solves
 mkdir -p gpurun_out
 S=gpurun_out/status.txt; : > $S
-rm -f gpurun_out/kbench.jsonl gpurun_out/*.ncu-rep
-timeout 900 python -m pytest tests -m gpu -q -k "async_px or deferred or persistent" > gpurun_out/pytest_apx.log 2>&1; echo pytest_apx=$? >> $S
-for ap in 0 1; do for op in poisson mom_v; do CHB_PXASYNC=$ap timeout 300 python scripts/kbench.py --solve $op | sed "s/^{/{\"apx\": $ap, /" >> gpurun_out/kbench.jsonl 2>> gpurun_out/kbench.err; done; done
-CHB_PXASYNC=1 timeout 900 python bench.py > gpurun_out/bench_apx.log 2>&1; echo bench_apx=$? >> $S
+rm -f gpurun_out/kbench.jsonl
+for ny in 4096 2048 1024 512; do for op in poisson mom_v; do timeout 300 python scripts/kbench.py --nx 4096 --ny $ny --solve $op >> gpurun_out/kbench.jsonl 2>> gpurun_out/kbench.err; done; done
+echo done >> $S

@@ -22,8 +22,12 @@ ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--warmup", type=int, default=1)
 ap.add_argument("--stride", type=int, default=4)
 ap.add_argument("--solve", default=None)
+ap.add_argument("--nx", type=int, default=0, help="override the config's grid (e.g. one rank's slab)")
+ap.add_argument("--ny", type=int, default=0)
 a = ap.parse_args()
-cfg = CONFIGS[a.config]
+cfg = dict(CONFIGS[a.config])
+if a.nx and a.ny:
+    cfg.update(nx=a.nx, ny=a.ny, name=f"{a.nx}x{a.ny}")
 sim = Simulation(cfg["nx"], cfg["ny"], dt=cfg["dt"])
 sim.set_fields(**initial_fields(cfg["nx"], cfg["ny"], seed=0))
 if a.solve:
