@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libch_b200.so")
+LIB_PATH = os.environ.get("CHB_LIB") or os.path.join(HERE, "libch_b200.so")  # override: experiments
 
 CH_OK, CH_ERR_ARG, CH_ERR_CUDA, CH_ERR_NOT_CONVERGED, CH_ERR_BREAKDOWN, CH_ERR_COMM = range(6)
 CH_HOST, CH_DEVICE = 0, 1
