@@ -163,7 +163,8 @@ def run_ours(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     cfg = CONFIGS[args.config]
     nx, ny = cfg["nx"], cfg["ny"]
-    sp = SimParams(dt=cfg["dt"], ch_solver=args.ch_solver)
+    # refine: CG restarts until the TRUE residual meets rtol (R21)
+    sp = SimParams(dt=cfg["dt"], ch_solver=args.ch_solver, refine=args.refine)
     sim = Simulation(nx, ny, sp, rank=rank, nranks=world, device=local_rank)
     if world > 1:
         sim.comm_init(share_unique_id(dist, rank))
@@ -260,7 +261,8 @@ def run_ours(args, rank, world, local_rank):
                 "data": "synthetic",
                 "config": {"workload": cfg["name"], "nx": nx, "ny": ny, "dt": cfg["dt"],
                            "parallelism": f"slab-y x{world}", "ch_solver": args.ch_solver,
-                           "rtol": sp.rtol, "l2": "inputs larger than L2 (134 MB per field)",
+                           "rtol": sp.rtol, "true_residual_refine": sp.refine,
+                           "l2": "inputs larger than L2 (134 MB per field)",
                            "krylov_iters_per_step": iters_step},
                 "roofline": roof, "kernels": per_class, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": st["launches"] * world, "clocks": clk.summary()}
@@ -281,6 +283,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ch-solver", default="bicgstab", choices=["bicgstab", "gmres"])
     ap.add_argument("--timing-stride", type=int, default=16)
+    ap.add_argument("--refine", type=int, default=2,
+                    help="CG true-residual refinement restarts (0: recursive residual only)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -108,7 +108,10 @@ typedef struct ch_params {
   int32_t maxit;   /* iteration cap per solve                      */
   int32_t ch_solver;      /* CH_SOLVER_*                           */
   int32_t gmres_restart;  /* m of GMRES(m), 1..64                  */
-  int32_t reserved;
+  int32_t refine;  /* symmetric (CG) solves: up to `refine` restarts  */
+                   /* from the converged x until the TRUE residual   */
+                   /* ||b - A x|| <= rtol ||b|| (0 = stop on the     */
+                   /* method's recursive residual, PETSc's default)  */
 } ch_params;
 
 typedef struct ch_stats {

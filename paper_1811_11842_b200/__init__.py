@@ -44,6 +44,7 @@ class SimParams:
     maxit: int = 200000
     ch_solver: str = "bicgstab"
     gmres_restart: int = 30
+    refine: int = 0
 
     def to_c(self) -> _lib.Params:
         p = _lib.Params()
@@ -52,7 +53,6 @@ class SimParams:
             if f.name == "ch_solver":
                 v = _lib.SOLVERS[v]
             setattr(p, f.name, v)
-        p.reserved = 0
         return p
 
 

@@ -33,7 +33,7 @@ class Params(C.Structure):
                                           "A", "Ds", "Re_s", "Re_n", "rho_n", "rho_s", "lid_u",
                                           "rtol")] + \
                [("maxit", C.c_int32), ("ch_solver", C.c_int32), ("gmres_restart", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("refine", C.c_int32)]
 
 
 class Stats(C.Structure):

@@ -80,12 +80,14 @@ def test_one_step_matches_oracle(nx, ny):
         assert st["resid_last"][sysname] <= 1e-12
 
 
+@pytest.mark.parametrize("refine", [0, 2])
 @pytest.mark.parametrize("nx,ny", [(64, 64), (130, 70)])
-def test_one_step_at_north_star_rtol(nx, ny):
+def test_one_step_at_north_star_rtol(nx, ny, refine):
     """At north_star's rtol 1e-10 every field matches within 1e-9 plus the
     oracle's own stopping-point sensitivity (R17), the iteration counts agree
-    within 2 and every solve reaches 1e-10."""
-    got, ref, st, iters = _run_both(nx, ny, 1)
+    within 2 (+ the few restart iterations with true-residual refinement,
+    R21) and every solve reaches 1e-10."""
+    got, ref, st, iters = _run_both(nx, ny, 1, refine=refine)
     tr = _oracle_truncation(nx, ny)
     for k in FIELDS:
         assert _rel(got[k], ref[k]) <= 1e-9 + tr[k], (k, _rel(got[k], ref[k]), tr[k])
@@ -93,7 +95,8 @@ def test_one_step_at_north_star_rtol(nx, ny):
         assert tr[k] < 1e-9
         assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
     for sysname, n in iters[-1].items():
-        assert abs(st["iters_last"][sysname] - n) <= 2, (sysname, st["iters_last"], iters[-1])
+        slack = 2 + (8 if refine and sysname != "ch" else 0)
+        assert -2 <= st["iters_last"][sysname] - n <= slack, (sysname, st["iters_last"], iters[-1])
         assert st["resid_last"][sysname] <= 1e-10
 
 
@@ -351,14 +354,14 @@ def test_isolated_solve_matches_oracle(op, nx, ny):
         assert abs(it_gpu - it_ref) <= 2, (it_gpu, it_ref)
 
 
-def _true_residual_4096(op, kind, variant, monkeypatch):
+def _true_residual_4096(op, kind, variant, monkeypatch, refine=0):
     import torch
     from paper_1811_11842_b200 import Simulation
     from workloads import initial_fields
     monkeypatch.setenv("CHB_VEC", variant)
     n = 4096
     f = initial_fields(n, n, seed=0)
-    sim = Simulation(n, n)
+    sim = Simulation(n, n, refine=refine)
     sim.set_fields(**f)
     if kind == "random":
         g = torch.Generator(device="cuda").manual_seed(3)
@@ -558,3 +561,18 @@ def test_odd_and_tiny_grids_match_oracle(nx, ny):
     got, ref, st, iters = _run_both(nx, ny, 1, rtol=1e-12, Lambda=1e-5)
     for k in FIELDS:
         assert _rel(got[k], ref[k]) <= 1e-9, (nx, ny, k, _rel(got[k], ref[k]))
+
+
+
+@pytest.mark.parametrize("op", ["poisson", "mom_u"])
+def test_full_size_true_residual_refinement(op, monkeypatch, record_property):
+    """params.refine: restarting CG from the converged x until its own
+    initialisation (b - A x from scratch) already meets rtol drives the TRUE
+    residual to rtol at 4096^2 even for a smooth right-hand side."""
+    base = _true_residual_4096(op, "smooth", "3", monkeypatch)
+    ref = _true_residual_4096(op, "smooth", "3", monkeypatch, refine=4)
+    record_property("iters_base", base[2])
+    record_property("iters_refined", ref[2])
+    print("true residual, iterations: plain", base, "refined", ref)
+    assert ref[0] <= 2e-10, ref
+    assert ref[2] >= base[2]
