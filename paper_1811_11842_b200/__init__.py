@@ -25,7 +25,8 @@ __all__ = ["Simulation", "SimParams", "CHError", "unique_id"]
 
 @dataclass
 class SimParams:
-    """ch_params with PAPER.md §5 defaults (lines 271-274), R8-R10, R13."""
+    """ch_params with PAPER.md §5 defaults (lines 271-274), DESIGN.md R8-R10, R13;
+    refine = CG restarts until the true residual meets rtol (R21, 0 = off)."""
     dt: float = 1e-4
     Gamma1: float = 33.467
     Gamma2: float = 1.25e6
