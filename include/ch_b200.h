@@ -146,8 +146,12 @@ enum {
 };
 
 /* Create a handle: allocates the rank's slab state and workspace on
- * grid->device.  Fields start zero except c = 1.  Returns NULL on error with
- * *status set (status may be NULL). */
+ * grid->device (about 41 fields of (nrows + 4) x pitch doubles at the
+ * default CG block length, halved automatically if device memory is short).
+ * Fields start zero except c = 1.  Parameters are copied (the caller keeps
+ * ownership of *grid and *params).  Returns NULL on error with *status set
+ * (status may be NULL): CH_ERR_ARG for an invalid grid / parameter set,
+ * CH_ERR_CUDA if the device cannot be used or memory runs out. */
 ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status);
 
 /* Multi-process runs (grid->nranks > 1): join the NCCL clique.  `id` is the
@@ -178,8 +182,22 @@ int ch_set_fields(ch_handle* h, const double* phi, const double* c, const double
                   const double* v, const double* p, int where);
 int ch_set_field(ch_handle* h, int field, const double* src, int where);
 
-/* Advance nsteps time steps (§4).  Stream-ordered; returns after
- * the last solve's convergence has been observed on the host. */
+/* Advance nsteps time steps of the semi-implicit scheme (§4, lines
+ * 117-151; splitting order DESIGN.md R1), each step:
+ *   1. phi* = (3 phi^n - phi^{n-1}) / 2; Cahn-Hilliard system (Eq. 16 4th
+ *      line with Eq. 4-5, Crank-Nicolson on the Gamma1 term) solved by
+ *      BiCGStab / GMRES(m) with Jacobi;
+ *   2. nutrient c^{n+1} (Eq. 16 3rd line, Eq. 7), Jacobi-PCG;
+ *   3. intermediate velocity u*, v* (Eq. 18-19, R6-R7), Jacobi-PCG each;
+ *   4. pressure -div(1/rho grad p) = div u* (Eq. 20) with the constant null
+ *      space removed (Listing 5), Jacobi-PCG;
+ *   5. projection v^{n+1} = u* + (1/rho) grad p (Eq. 21).
+ * Every solve stops at ||r|| <= rtol ||b|| (R13, R21 for params.refine).
+ * All device work is ordered on the library stream; the call returns when
+ * the last step is complete.  On error (CH_ERR_NOT_CONVERGED,
+ * CH_ERR_BREAKDOWN, CH_ERR_CUDA, CH_ERR_COMM) ch_last_error names the
+ * system and the steps completed before it remain in the state; stats say
+ * which system failed (iters_last / resid_last). */
 int ch_step(ch_handle* h, int nsteps);
 
 /* Copy the state out (NULL pointers skipped).  CH_HOST copies synchronise. */

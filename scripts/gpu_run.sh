@@ -1,7 +1,3 @@
 mkdir -p gpurun_out
 S=gpurun_out/status.txt; : > $S
-rm -f gpurun_out/kbench.jsonl
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$? >> $S
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> $S
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$? >> $S
-for op in poisson mom_v; do timeout 300 python scripts/kbench.py --solve $op >> gpurun_out/kbench.jsonl 2>> gpurun_out/kbench.err; done
+for c in 0 1 2; do CHB_PERSIST=1 timeout 900 python bench.py --config $c --no-cpu > gpurun_out/bench_p_c$c.log 2>&1; echo bench_p_c$c=$? >> $S; done
