@@ -244,15 +244,22 @@ int halo_local(ch_handle* h, int id, int w) {
   return CH_OK;
 }
 
+int halo(ch_handle* h, int id, int w);
+
 // One CG iteration's communication: partial-sum combination (finalize) and
 // the ghost rows of z' (2) and s (1).  Across processes the allgather and the
 // halo rows go in ONE NCCL group.
 int iter_exchange(ch_handle* h, int fin, int sys, int K, int zid, int sid) {
   if (h->nslabs_total == 1) return CH_OK;
-  if (!h->comm) {
+  static int grouped = -1;  // env CHB_NCCL_GROUP=0: separate NCCL calls (safety valve)
+  if (grouped < 0) {
+    const char* e = getenv("CHB_NCCL_GROUP");
+    grouped = e ? atoi(e) != 0 : 1;
+  }
+  if (!h->comm || !grouped) {
     TRY(fin_slabs(h, fin, sys, K));
-    TRY(halo_local(h, zid, 2));
-    return halo_local(h, sid, 1);
+    TRY(halo(h, zid, 2));
+    return halo(h, sid, 1);
   }
   TRY(halo_local(h, zid, 2));
   TRY(halo_local(h, sid, 1));
