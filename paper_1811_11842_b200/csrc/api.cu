@@ -86,6 +86,7 @@ struct ch_handle {
                               // reduced at ch_create if the z history would not fit
   double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
   double* gm_host = nullptr;  // pinned mirror
+  int cg3 = 1;                // single-reduction CG: three-term z recurrence (env CHB_CG3)
   int vec = 3;                // CG: 3 single-reduction fused TMA sweep; two-kernel HS-CG with
                               // 2 TMA ring, 1 register pipeline, 0 scalar (env CHB_VEC)
   int strip2 = 0;             // rows per strip, 0 = one resident wave (env CHB_STRIP)
@@ -247,8 +248,8 @@ int halo_local(ch_handle* h, int id, int w) {
 int halo(ch_handle* h, int id, int w);
 
 // One CG iteration's communication: partial-sum combination (finalize) and
-// the ghost rows of z' (2) and s (1).  Across processes the allgather and the
-// halo rows go in ONE NCCL group.
+// the ghost rows of z' (2) and s (1; none for the three-term recurrence, sid < 0).
+// Across processes the allgather and the halo rows go in ONE NCCL group.
 int iter_exchange(ch_handle* h, int fin, int sys, int K, int zid, int sid) {
   if (h->nslabs_total == 1) return CH_OK;
   static int grouped = -1;  // env CHB_NCCL_GROUP=0: separate NCCL calls (safety valve)
@@ -259,15 +260,16 @@ int iter_exchange(ch_handle* h, int fin, int sys, int K, int zid, int sid) {
   if (!h->comm || !grouped) {
     TRY(fin_slabs(h, fin, sys, K));
     TRY(halo(h, zid, 2));
-    return halo(h, sid, 1);
+    return sid >= 0 ? halo(h, sid, 1) : CH_OK;
   }
   TRY(halo_local(h, zid, 2));
-  TRY(halo_local(h, sid, 1));
+  if (sid >= 0) TRY(halo_local(h, sid, 1));
   const Slab& first = h->sl.front();
   const Slab& last = h->sl.back();
   HaloSpec hs[2] = {{first.a[zid], last.a[zid], last.g.nyl, 2},
-                    {first.a[sid], last.a[sid], last.g.nyl, 1}};
-  if (comm_iter_exchange(h->comm, h->tot_local, h->tot, (size_t)h->S * 8, hs, 2,
+                    {sid >= 0 ? first.a[sid] : nullptr, sid >= 0 ? last.a[sid] : nullptr,
+                     last.g.nyl, 1}};
+  if (comm_iter_exchange(h->comm, h->tot_local, h->tot, (size_t)h->S * 8, hs, sid >= 0 ? 2 : 1,
                          first.g.pitch, h->st) != 0) {
     h->err = "comm iteration exchange failed";
     return CH_ERR_COMM;
@@ -558,9 +560,10 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
     // algorithmic bytes of the launch: K sweeps + the in-kernel p/x updates
     const long K = h->sch[sys].iter;
     if (!h->tm.pending.empty() && h->tm.pending.back().kc == kc_sys)
-      h->tm.pending.back().bytes = (cgs_bytes(kind, 0) * (double)K +
+      h->tm.pending.back().bytes = (cgs_bytes(kind, 0, 0) * (double)K +
                                     8.0 * (m + 4) * (double)(K / m)) * cells;
   } else {
+  const int tt = h->cg3 && NZ >= 3;
   long k = 0;
   int chunk = 4;
   for (;;) {
@@ -568,13 +571,17 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
       const int first = (k == 0), dir = (k & 1) ? -1 : 1;
       if (apx && (k + 1) % m == 0 && k + 1 >= 2 * m)  // block (k+1)/m - 2's p/x must be done
         CK(cudaStreamWaitEvent(h->st, h->pxev[((k + 1) / m - 2) & 3], 0));
-      const int zi = Zr[k % NZ], zo = Zr[(k + 1) % NZ], si = S[(k + 1) & 1], so = S[k & 1];
+      const int zi = Zr[k % NZ], zo = Zr[(k + 1) % NZ];
+      // three-term: the sweep reads z_{k-1} (still in the ring) instead of s_{k-1}
+      // and writes no s
+      const int si = tt ? Zr[(k + NZ - 1) % NZ] : S[(k + 1) & 1], so = tt ? -1 : S[k & 1];
       {
-        KTime kt(h, kc_sys, cgs_bytes(kind, first) * cells, k + 1);
+        KTime kt(h, kc_sys, cgs_bytes(kind, first, tt) * cells, k + 1);
         for (int s = 0; s < h->S; ++s) {
           Slab& sl = h->sl[s];
-          launch_cgs_iter(opdesc(h, kind, sl), sl.g, sl.a[zi], sl.a[zo], sl.a[si], sl.a[so],
-                          first, dir, rargs(h, FIN_CGS, sys, s), h->st);
+          launch_cgs_iter(opdesc(h, kind, sl), sl.g, sl.a[zi], sl.a[zo], sl.a[si],
+                          so >= 0 ? sl.a[so] : nullptr, first, dir, tt,
+                          rargs(h, FIN_CGS, sys, s), h->st);
         }
       }
       TRY(iter_exchange(h, FIN_CGS, sys, 3, zo, so));
@@ -1124,6 +1131,7 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   h->S = S;
   h->nslabs_total = total;
   if (const char* e = getenv("CHB_VEC")) h->vec = atoi(e);
+  if (const char* e = getenv("CHB_CG3")) h->cg3 = atoi(e) != 0;
   if (const char* e = getenv("CHB_STRIP")) h->strip2 = std::max(0, atoi(e));
   if (const char* e = getenv("CHB_PDL")) h->pdl = atoi(e) != 0;
   if (const char* e = getenv("CHB_DEFER")) h->cg_defer = std::min(std::max(2, atoi(e)), CGM);

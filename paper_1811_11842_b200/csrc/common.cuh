@@ -214,6 +214,8 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
       s->alpha = s->rho / t[0];
       s->beta = 0.0;
       s->aux[0] = 0.0;
+      s->aux[4] = s->alpha;  // three-term z recurrence: gamma_0 = alpha_0, omega_1 = 1
+      s->aux[5] = 1.0;
       cgs_coef_update(fc.tab, fc.m, 0, s->alpha, 0.0);
       break;
     }
@@ -227,6 +229,13 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
       const double beta = t[0] / s->rho;
       const double den = t[2] - beta * t[0] / s->alpha;
       if (bad(den)) { s->status = 1; s->done = 1; break; }
+      // three-term z recurrence (Concus-Golub-O'Leary form, kernels_cgs.cu):
+      // gamma' = mu'/nu', omega' = 1 / (1 - (gamma'/gamma) (mu'/mu) / omega)
+      const double gnew = t[0] / t[2];
+      const double om = 1.0 / (1.0 - (gnew / s->aux[4]) * (t[0] / s->rho) / s->aux[5]);
+      if (bad(gnew) || !(fabs(om) < 1e300)) { s->status = 1; s->done = 1; break; }
+      s->aux[4] = gnew;
+      s->aux[5] = om;
       s->aux[0] = s->alpha;  // alpha_{i} for the in-sweep x update over pairs
       s->beta = beta;
       s->alpha = t[0] / den;

@@ -60,8 +60,9 @@ void launch_op5_apply(const OpDesc& d, const Geom& g, const double* x, double* y
 void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace, int odd_only,
                        const RedArgs& ra, cudaStream_t st);
 // single-reduction CG (kernels_cgs.cu), even nx only
+// tt = 1: three-term z recurrence (si = z_{i-1}, so unused); 0: s = A p recurrence
 void launch_cgs_iter(const OpDesc& d, const Geom& g, const double* zi, double* zo,
-                     const double* si, double* so, int first, int dir, const RedArgs& ra,
+                     const double* si, double* so, int first, int dir, int tt, const RedArgs& ra,
                      cudaStream_t st);
 struct ZList {
   const double* z[CGM];
@@ -86,7 +87,7 @@ struct PArgs {
 int launch_cgs_persist(const OpDesc& d, const Geom& g, const PArgs& pa, cudaStream_t st);
 void launch_cgs_delta0(const OpDesc& d, const Geom& g, const double* z, const RedArgs& ra,
                        cudaStream_t st);
-double cgs_bytes(int kind, int first);
+double cgs_bytes(int kind, int first, int tt);
 void launch_sum(const Geom& g, const double* x, const RedArgs& ra, cudaStream_t st);
 void launch_sub_mean(const Geom& g, double* x, const KScal* sc, cudaStream_t st);
 void launch_finalize_slabs(const double* tot, int nslabs, int K, const RedArgs& ra,

@@ -1,3 +1,7 @@
 mkdir -p gpurun_out
 S=gpurun_out/status.txt; : > $S
-for c in 0 1 2; do CHB_PERSIST=1 timeout 900 python bench.py --config $c --no-cpu > gpurun_out/bench_p_c$c.log 2>&1; echo bench_p_c$c=$? >> $S; done
+rm -f gpurun_out/kbench.jsonl
+for v in base rcp ldrow nopf; do
+  if [ $v = base ]; then L=""; else L=$PWD/paper_1811_11842_b200/libch_b200_$v.so; fi
+  for op in poisson mom_v; do CHB_LIB=$L timeout 300 python scripts/kbench.py --solve $op | sed "s/^{/{\"lib\": \"$v\", /" >> gpurun_out/kbench.jsonl 2>> gpurun_out/kbench.err; echo $v$op=$? >> $S; done
+done

@@ -114,14 +114,17 @@ def test_bicgstab_nontrivial_ch_system():
         assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
 
 
+@pytest.mark.parametrize("cg3", ["1", "0"])
 @pytest.mark.parametrize("slabs", [2, 3])
-def test_virtual_slabs_match_single_slab(slabs):
-    """Slab decomposition in y with halo exchange reproduces the 1-slab step.
+def test_virtual_slabs_match_single_slab(slabs, cg3, monkeypatch):
+    """Slab decomposition in y with halo exchange reproduces the 1-slab step
+    (CG: three-term z recurrence, z halos only; and s recurrence, z + s halos).
     The Krylov dot products sum in a different order per decomposition, so the
     comparison runs the solves to rtol = 1e-13 (differences are then rounding
     propagated through ~200 CG iterations, not solver tolerance)."""
     from paper_1811_11842_b200 import Simulation
     from workloads import initial_fields
+    monkeypatch.setenv("CHB_CG3", cg3)
     f = initial_fields(40, 36, seed=4)
     out, its = [], []
     for s in (1, slabs):
@@ -295,6 +298,26 @@ def test_cg_kernel_variants_short_strips(variant, strip, monkeypatch):
     got, ref, _, _ = _run_both(64, 40, 1, rtol=1e-12)
     for k in FIELDS:
         assert _rel(got[k], ref[k]) <= 1e-9, (variant, k, _rel(got[k], ref[k]))
+
+
+@pytest.mark.parametrize("cg3", ["0", "1"])
+@pytest.mark.parametrize("nx,ny,strip", [(64, 48, "0"), (300, 70, "0"), (64, 40, "1"),
+                                         (64, 40, "2")])
+def test_single_reduction_recurrences(cg3, nx, ny, strip, monkeypatch):
+    """Single-reduction CG with the three-term z recurrence (1, default: the
+    sweep reads z_{i-1}, no s vector) and with the s = A p recurrence (0):
+    both match the oracle's Hestenes-Stiefel CG fields and iteration counts,
+    on ragged chunks and on 1-2-row strips (halo rows of z_{i-1} at every
+    strip edge)."""
+    monkeypatch.setenv("CHB_VEC", "3")
+    monkeypatch.setenv("CHB_CG3", cg3)
+    if strip != "0":
+        monkeypatch.setenv("CHB_STRIP", strip)
+    got, ref, st, iters = _run_both(nx, ny, 1, rtol=1e-12)
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (cg3, k, _rel(got[k], ref[k]))
+    for sysname in ("nutrient", "u", "v", "p"):
+        assert abs(st["iters_last"][sysname] - iters[-1][sysname]) <= 2, (sysname, st, iters)
 
 
 # ------------------------------------------------------------ isolated solves
