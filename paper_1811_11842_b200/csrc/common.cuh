@@ -132,9 +132,46 @@ __device__ inline void cgs_coef_update(double* tab, int m, int i, double alpha, 
   T[CG_N] = (double)(j + 1);
 }
 
+// The same update by the 32 lanes of one warp, lane k owning slot k (CGM ==
+// 32): two dependent L2 round trips instead of ~2 j serial ones on the
+// per-iteration critical path (the last CTA's finalize).
+static_assert(CGM == 32, "one lane per deferred z slot");
+__device__ inline void cgs_coef_update_warp(double* tab, int m, int i, double alpha, double beta,
+                                            int lane) {
+  if (!tab || m <= 0) return;
+  double* T = tab + ((i / m) & 1) * CGT;
+  const int j = i % m, k = lane;
+  double pz = 0.0, cz = 0.0, cpp = 1.0, cxp = 0.0;
+  if (j != 0) {
+    pz = T[CG_PZ + k];
+    cz = T[CG_CZ + k];
+    cpp = T[CG_CPP];
+    cxp = T[CG_CXP];
+  }
+  if (k < j) pz *= beta;
+  if (k == j) pz = 1.0;
+  if (k <= j) cz += alpha * pz;
+  T[CG_PZ + k] = pz;
+  T[CG_CZ + k] = cz;
+  if (k == 0) {
+    cpp *= beta;
+    cxp += alpha * cpp;
+    T[CG_CPP] = cpp;
+    T[CG_CXP] = cxp;
+    T[CG_N] = (double)(j + 1);
+  }
+}
+
+// A deferred coefficient-table update requested by finalize (see finalize_warp).
+struct CoefReq {
+  int valid, i;
+  double alpha, beta;
+};
+
 __device__ __forceinline__ bool bad(double x) { return !(x == x) || x == 0.0; }
 
-__device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx& fc) {
+__device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx& fc,
+                                CoefReq* req = nullptr) {
   switch (fin) {
     case FIN_CG_INIT: {
       s->bb = t[0];
@@ -216,7 +253,8 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
       s->aux[0] = 0.0;
       s->aux[4] = s->alpha;  // three-term z recurrence: gamma_0 = alpha_0, omega_1 = 1
       s->aux[5] = 1.0;
-      cgs_coef_update(fc.tab, fc.m, 0, s->alpha, 0.0);
+      if (req) *req = CoefReq{1, 0, s->alpha, 0.0};
+      else cgs_coef_update(fc.tab, fc.m, 0, s->alpha, 0.0);
       break;
     }
     case FIN_CGS: {
@@ -240,7 +278,8 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
       s->beta = beta;
       s->alpha = t[0] / den;
       s->rho = t[0];
-      cgs_coef_update(fc.tab, fc.m, s->iter, s->alpha, beta);
+      if (req) *req = CoefReq{1, s->iter, s->alpha, beta};
+      else cgs_coef_update(fc.tab, fc.m, s->iter, s->alpha, beta);
       break;
     }
     case FIN_STORE: {
@@ -250,6 +289,20 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
     default:
       break;
   }
+}
+
+// finalize() run by all 32 lanes of a warp (t valid in lane 0): lane 0 updates
+// the scalars, the lanes then share the coefficient-table update.
+__device__ inline void finalize_warp(int fin, const double* t, KScal* s, const FinCtx& fc) {
+  const int lane = threadIdx.x & 31;
+  CoefReq req{0, 0, 0.0, 0.0};
+  if (lane == 0) finalize(fin, t, s, fc, &req);
+  req.valid = __shfl_sync(FULL, req.valid, 0);
+  if (!req.valid) return;
+  req.i = __shfl_sync(FULL, req.i, 0);
+  req.alpha = __shfl_sync(FULL, req.alpha, 0);
+  req.beta = __shfl_sync(FULL, req.beta, 0);
+  cgs_coef_update_warp(fc.tab, fc.m, req.i, req.alpha, req.beta, lane);
 }
 
 // Reduction plumbing: every block writes K partial sums; the last block to
@@ -310,7 +363,7 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
     if (lane == 0) sm[wid][k] = t;
   }
   __syncthreads();
-  if (tid != 0) return;
+  if (wid != 0) return;
   double res[K > 0 ? K : 1];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -318,14 +371,12 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
     for (int w = 0; w < nw; ++w) t += sm[w][k];
     res[k] = t;
   }
-  {
-    *ra.ticket = 0u;
-    if (ra.inline_fin) {
-      finalize(ra.fin, res, ra.sc, ra.fc);
-    } else {
+  if (lane == 0) *ra.ticket = 0u;
+  if (ra.inline_fin) {
+    finalize_warp(ra.fin, res, ra.sc, ra.fc);
+  } else if (lane == 0) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) ra.tot[ra.slab * 8 + k] = res[k];
-    }
+    for (int k = 0; k < K; ++k) ra.tot[ra.slab * 8 + k] = res[k];
   }
 }
 

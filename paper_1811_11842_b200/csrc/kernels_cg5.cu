@@ -556,7 +556,8 @@ __global__ void __launch_bounds__(256) k_sub_mean(Geom g, double* __restrict__ x
 }
 
 __global__ void k_finalize_slabs(const double* tot, int nslabs, int K, RedArgs ra) {
-  if (threadIdx.x != 0) return;
+  // one warp (launch_finalize_slabs): lane 0 finalizes, the lanes share the
+  // coefficient-table update
   // iteration-phase finalizers are no-ops once the solve is done (their slab
   // kernels returned early and the totals are stale); BiCGStab's omega phase
   // is skipped after a half-step convergence
@@ -571,7 +572,7 @@ __global__ void k_finalize_slabs(const double* tot, int nslabs, int K, RedArgs r
     for (int i = 0; i < nslabs; ++i) s += tot[i * 8 + k];
     t[k] = s;
   }
-  finalize(ra.fin, t, ra.sc, ra.fc);
+  finalize_warp(ra.fin, t, ra.sc, ra.fc);
 }
 
 // ============================================================== launchers
