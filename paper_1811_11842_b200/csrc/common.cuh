@@ -305,6 +305,133 @@ __device__ inline void finalize_warp(int fin, const double* t, KScal* s, const F
   cgs_coef_update_warp(fc.tab, fc.m, req.i, req.alpha, req.beta, lane);
 }
 
+// FIN_CGS with its scalar inputs prefetched (CgsPre, loaded by the sweep
+// while its ring fills) and its coefficient-table slots loaded together with
+// the partial sums: the last CTA's finalize then adds no global round trip
+// to the critical path between sweeps.  Run by all 32 lanes of warp 0 (the
+// scalar logic redundantly, lane 0 stores the scalars, lane k table slot k);
+// same arithmetic and outcomes as finalize(FIN_CGS).
+struct CgsPre {
+  double rho, alpha, aux4, aux5, tol2;
+  int iter, maxit;
+};
+
+__device__ inline void cgs_prefetch(CgsPre& p, const KScal* s, int lane) {
+  if (lane == 0) {
+    p.iter = __ldcg(&s->iter);
+    p.maxit = __ldcg(&s->maxit);
+    p.rho = __ldcg(&s->rho);
+    p.alpha = __ldcg(&s->alpha);
+    p.aux4 = __ldcg(&s->aux[4]);
+    p.aux5 = __ldcg(&s->aux[5]);
+    p.tol2 = __ldcg(&s->tol2);
+  }
+}
+
+// table slot `lane` (+ CPP, CXP) of the iteration the finalize will record
+struct CgsSlot {
+  double pz, cz, cpp, cxp;
+};
+__device__ inline CgsSlot cgs_slot_load(const CgsPre& p, const FinCtx& fc, int lane) {
+  CgsSlot o{0.0, 0.0, 1.0, 0.0};
+  if (!fc.tab || fc.m <= 0) return o;
+  const int i = p.iter + 1;
+  const double* T = fc.tab + ((i / fc.m) & 1) * CGT;
+  o.pz = __ldcg(T + CG_PZ + lane);
+  o.cz = __ldcg(T + CG_CZ + lane);
+  o.cpp = __ldcg(T + CG_CPP);
+  o.cxp = __ldcg(T + CG_CXP);
+  return o;
+}
+
+__device__ inline void finalize_cgs_pre(const double* t, const CgsPre& p, const CgsSlot& sl,
+                                        KScal* s, const FinCtx& fc, int lane) {
+  const int iter = p.iter + 1;
+  int done = 0, status = 0;
+  double beta = 0.0, alpha = 0.0, gnew = 0.0, om = 0.0;
+  if (t[1] <= p.tol2) {
+    done = 1;
+  } else if (iter >= p.maxit) {
+    status = 2;
+    done = 1;
+  } else if (bad(t[0]) || bad(p.rho) || bad(p.alpha)) {
+    status = 1;
+    done = 1;
+  } else {
+    beta = t[0] / p.rho;
+    const double den = t[2] - beta * t[0] / p.alpha;
+    gnew = t[0] / t[2];
+    om = 1.0 / (1.0 - (gnew / p.aux4) * (t[0] / p.rho) / p.aux5);
+    if (bad(den) || bad(gnew) || !(fabs(om) < 1e300)) {
+      status = 1;
+      done = 1;
+    } else {
+      alpha = t[0] / den;
+    }
+  }
+  if (lane == 0) {
+    s->iter = iter;
+    s->rr = t[1];
+    if (done) {
+      if (status) s->status = status;
+      s->done = 1;
+    } else {
+      s->aux[4] = gnew;
+      s->aux[5] = om;
+      s->aux[0] = p.alpha;
+      s->beta = beta;
+      s->alpha = alpha;
+      s->rho = t[0];
+    }
+  }
+  if (done || !fc.tab || fc.m <= 0) return;
+  double* T = fc.tab + ((iter / fc.m) & 1) * CGT;
+  const int j = iter % fc.m, k = lane;
+  double pz = 0.0, cz = 0.0, cpp = 1.0, cxp = 0.0;
+  if (j != 0) {
+    pz = sl.pz;
+    cz = sl.cz;
+    cpp = sl.cpp;
+    cxp = sl.cxp;
+  }
+  if (k < j) pz *= beta;
+  if (k == j) pz = 1.0;
+  if (k <= j) cz += alpha * pz;
+  T[CG_PZ + k] = pz;
+  T[CG_CZ + k] = cz;
+  if (k == 0) {
+    cpp *= beta;
+    cxp += alpha * cpp;
+    T[CG_CPP] = cpp;
+    T[CG_CXP] = cxp;
+    T[CG_N] = (double)(j + 1);
+  }
+}
+
+#ifdef CHB_TRACE
+// (kernels_cgs.cu) timing trace of the last k_cgs_iter launch (experiments only): per CTA
+// globaltimer at entry, after griddepcontrol.wait, ring ready, loop end,
+// after the reduction (+ finalize in the last CTA); clock64 of the same points
+__device__ unsigned long long chb_trace[8192 * 16];
+__device__ __forceinline__ void trace_now(unsigned long long& gt, unsigned long long& ck) {
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(ck));
+}
+__device__ __forceinline__ void trace_put(int i, unsigned long long gt, unsigned long long ck) {
+  if (threadIdx.x != 0) return;
+  chb_trace[blockIdx.x * 16 + i] = gt;
+  chb_trace[blockIdx.x * 16 + 8 + i] = ck;
+}
+__device__ __forceinline__ void trace_pt(int i) {
+  unsigned long long gt, ck;
+  trace_now(gt, ck);
+  trace_put(i, gt, ck);
+}
+#define CHB_TP(i) trace_pt(i)
+#else
+#define CHB_TP(i) ((void)0)
+#endif
+
 // Reduction plumbing: every block writes K partial sums; the last block to
 // finish (atomic ticket) sums the partials in fixed block order (deterministic)
 // and either finalizes inline (single slab, single rank) or stores the slab
@@ -322,7 +449,8 @@ struct RedArgs {
 };
 
 template <int K>
-__device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedArgs& ra) {
+__device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedArgs& ra,
+                                                      const CgsPre* pre = nullptr) {
   __shared__ double sm[32][K > 0 ? K : 1];
   __shared__ int am_last;
   const int tid = threadIdx.x + threadIdx.y * blockDim.x;
@@ -332,6 +460,7 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
   const int nb = gridDim.x * gridDim.y;
 #pragma unroll
   for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  if (pre) CHB_TP(5);
   if (lane == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) sm[wid][k] = v[k];
@@ -345,24 +474,52 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
       if (lane == 0) ra.part[(size_t)bid * 8 + k] = t;
     }
     if (lane == 0) {
-      __threadfence();
-      unsigned prev = atomicAdd(ra.ticket, 1u);
+      // acq_rel ticket: releases this CTA's partials; the last arrival
+      // acquires everyone's (its threads' loads follow via the CTA barrier).
+      // Replaces __threadfence() (MEMBAR.SC.GPU + L1 invalidate) on both sides.
+      unsigned prev;
+      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                   : "=r"(prev) : "l"(ra.ticket) : "memory");
       am_last = (prev == (unsigned)(nb - 1));
     }
   }
   __syncthreads();
+  if (pre) CHB_TP(6);
   if (!am_last) return;
-  __threadfence();
+  CgsSlot slot{0.0, 0.0, 1.0, 0.0};
+  if (pre && wid == 0) slot = cgs_slot_load(*pre, ra.fc, lane);  // in flight with the partials
   // the last CTA sums the partials with all its warps (fixed partition and
   // order: deterministic), then one thread finalizes
+  {
+    // batches of 8 partials per thread, all loads in flight before the adds
+    // (a load-add chain costs one L2 round trip per partial: ~4 us at 740
+    // CTAs); fixed partition and order, so still deterministic
+    constexpr int U = 8;
+    const int nthr = nw * 32;
+    double t[K > 0 ? K : 1];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    double t = 0.0;
-    for (int b = wid * 32 + lane; b < nb; b += nw * 32) t += __ldcg(ra.part + (size_t)b * 8 + k);
-    t = warp_sum(t);
-    if (lane == 0) sm[wid][k] = t;
+    for (int k = 0; k < K; ++k) t[k] = 0.0;
+    for (int b0 = tid; b0 < nb; b0 += nthr * U) {
+      double x[U][K > 0 ? K : 1];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + u * nthr;
+#pragma unroll
+        for (int k = 0; k < K; ++k) x[u][k] = b < nb ? __ldcg(ra.part + (size_t)b * 8 + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < K; ++k) t[k] += x[u][k];
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double w = warp_sum(t[k]);
+      if (lane == 0) sm[wid][k] = w;
+    }
   }
   __syncthreads();
+  if (pre) CHB_TP(7);
   if (wid != 0) return;
   double res[K > 0 ? K : 1];
 #pragma unroll
@@ -373,7 +530,10 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
   }
   if (lane == 0) *ra.ticket = 0u;
   if (ra.inline_fin) {
-    finalize_warp(ra.fin, res, ra.sc, ra.fc);
+    if (pre && ra.fin == FIN_CGS)
+      finalize_cgs_pre(res, *pre, slot, ra.sc, ra.fc, lane);
+    else
+      finalize_warp(ra.fin, res, ra.sc, ra.fc);
   } else if (lane == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) ra.tot[ra.slab * 8 + k] = res[k];
