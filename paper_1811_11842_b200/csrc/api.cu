@@ -37,6 +37,7 @@ struct Slab {
   Geom g;
   double* a[A_N];
   std::vector<double*> V;  // GMRES basis (m + 1 vectors) + work
+  std::vector<void*> bases;  // cudaMalloc'd blocks behind a[] (arrays may start skewed)
 };
 
 struct Timer {
@@ -1076,8 +1077,7 @@ const char* ch_last_error(const ch_handle* h) { return h ? h->err.c_str() : "nul
 
 static void destroy_mem(ch_handle* h) {
   for (auto& s : h->sl) {
-    for (int i = 0; i < A_N; ++i)
-      if (s.a[i]) cudaFree(s.a[i]);
+    for (void* p : s.bases) cudaFree(p);
     for (double* p : s.V) cudaFree(p);
   }
   h->sl.clear();
@@ -1178,11 +1178,22 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
     sl.g.ihx2 = (double)G.nx * G.nx;
     sl.g.ihy2 = (double)G.ny * G.ny;
     for (int i = 0; i < A_N; ++i) sl.a[i] = nullptr;
-    // z history: only the m - 1 buffers the chosen block length needs
+    // z history: only the m - 1 buffers the chosen block length needs.
+    // Array i starts i * skew bytes (mod 64 KiB) into its block, so that the
+    // same cell of different arrays does not map to the same DRAM channel
+    // phase (env CHB_SKEW, bytes, multiple of 256)
     const int n_alloc = A_ZH0 + std::max(0, h->cg_defer - 1);
+    long skew = 0;
+    if (const char* e = getenv("CHB_SKEW")) skew = (atol(e) / 256) * 256;
+    if (skew < 0) skew = 0;
+    const size_t pad = skew ? 65536 : 0;
     for (int i = 0; i < n_alloc; ++i) {
-      if (cudaMalloc(&sl.a[i], h->arr_elems * sizeof(double)) != cudaSuccess)
+      void* base = nullptr;
+      if (cudaMalloc(&base, h->arr_elems * sizeof(double) + pad) != cudaSuccess)
         return fail(CH_ERR_CUDA, h, "cudaMalloc (out of device memory?)");
+      sl.bases.push_back(base);
+      const size_t off_b = skew ? ((size_t)i * (size_t)skew) % 65536 : 0;
+      sl.a[i] = reinterpret_cast<double*>(static_cast<char*>(base) + off_b);
       cudaMemset(sl.a[i], 0, h->arr_elems * sizeof(double));
     }
   }

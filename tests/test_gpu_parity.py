@@ -320,6 +320,15 @@ def test_single_reduction_recurrences(cg3, nx, ny, strip, monkeypatch):
         assert abs(st["iters_last"][sysname] - iters[-1][sysname]) <= 2, (sysname, st, iters)
 
 
+def test_skewed_array_starts(monkeypatch):
+    """CHB_SKEW: arrays start at staggered offsets inside their allocations
+    (DRAM-channel experiment); the step is unchanged."""
+    monkeypatch.setenv("CHB_SKEW", "4352")
+    got, ref, _, _ = _run_both(64, 48, 1, rtol=1e-12)
+    for k in FIELDS:
+        assert _rel(got[k], ref[k]) <= 1e-9, (k, _rel(got[k], ref[k]))
+
+
 # ------------------------------------------------------------ isolated solves
 def _solve_case(nx, ny, op, seed=0, **over):
     """GPU ch_solve vs the oracle's textbook Krylov on the assembled matrix,
