@@ -83,7 +83,7 @@ struct ch_handle {
   int cur_m = 0;              // block length of the solve in flight (0: cg_defer)
   cudaStream_t st2 = nullptr; // side stream of the asynchronous p/x updates
   cudaEvent_t pxev[5] = {};   // [0..3] p/x done per block (mod 4), [4] sweep-side marker
-  int cg_defer = 32;          // block length m (2..32) of the deferred p/x CG (env CHB_DEFER);
+  int cg_defer = 64;          // block length m (2..64) of the deferred p/x CG (env CHB_DEFER);
                               // reduced at ch_create if the z history would not fit
   double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
   double* gm_host = nullptr;  // pinned mirror

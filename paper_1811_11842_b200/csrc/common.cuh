@@ -111,8 +111,8 @@ struct FinCtx {
 //   x_{i+1} = x_{i0} + sum_k CZ[k] z_k + CXP p_{i0-1}
 // and the table follows the textbook updates p_i = z_i + beta_i p_{i-1},
 // x_{i+1} = x_i + alpha_i p_i exactly (only the summation order of x differs).
-constexpr int CGM = 32;  // max block length
-constexpr int CGT = 80;  // table stride (>= 2 CGM + 3)
+constexpr int CGM = 64;   // max block length
+constexpr int CGT = 136;  // table stride (>= 2 CGM + 3)
 enum { CG_PZ = 0, CG_CZ = CGM, CG_CPP = 2 * CGM, CG_CXP = 2 * CGM + 1, CG_N = 2 * CGM + 2 };
 
 __device__ inline void cgs_coef_update(double* tab, int m, int i, double alpha, double beta) {
@@ -132,28 +132,36 @@ __device__ inline void cgs_coef_update(double* tab, int m, int i, double alpha, 
   T[CG_N] = (double)(j + 1);
 }
 
-// The same update by the 32 lanes of one warp, lane k owning slot k (CGM ==
-// 32): two dependent L2 round trips instead of ~2 j serial ones on the
-// per-iteration critical path (the last CTA's finalize).
-static_assert(CGM == 32, "one lane per deferred z slot");
+// The same update by the 32 lanes of one warp, lane l owning slots l, l + 32
+// (CGM / 32 per lane): two dependent L2 round trips instead of ~2 j serial
+// ones on the per-iteration critical path (the last CTA's finalize).
+static_assert(CGM % 32 == 0 && CGM <= 64, "CGM / 32 deferred z slots per lane");
+constexpr int CGS_SLOTS = CGM / 32;
 __device__ inline void cgs_coef_update_warp(double* tab, int m, int i, double alpha, double beta,
                                             int lane) {
   if (!tab || m <= 0) return;
   double* T = tab + ((i / m) & 1) * CGT;
-  const int j = i % m, k = lane;
-  double pz = 0.0, cz = 0.0, cpp = 1.0, cxp = 0.0;
+  const int j = i % m;
+  double cpp = 1.0, cxp = 0.0;
   if (j != 0) {
-    pz = T[CG_PZ + k];
-    cz = T[CG_CZ + k];
     cpp = T[CG_CPP];
     cxp = T[CG_CXP];
   }
-  if (k < j) pz *= beta;
-  if (k == j) pz = 1.0;
-  if (k <= j) cz += alpha * pz;
-  T[CG_PZ + k] = pz;
-  T[CG_CZ + k] = cz;
-  if (k == 0) {
+#pragma unroll
+  for (int r = 0; r < CGS_SLOTS; ++r) {
+    const int k = lane + 32 * r;
+    double pz = 0.0, cz = 0.0;
+    if (j != 0) {
+      pz = T[CG_PZ + k];
+      cz = T[CG_CZ + k];
+    }
+    if (k < j) pz *= beta;
+    if (k == j) pz = 1.0;
+    if (k <= j) cz += alpha * pz;
+    T[CG_PZ + k] = pz;
+    T[CG_CZ + k] = cz;
+  }
+  if (lane == 0) {
     cpp *= beta;
     cxp += alpha * cpp;
     T[CG_CPP] = cpp;
@@ -330,15 +338,22 @@ __device__ inline void cgs_prefetch(CgsPre& p, const KScal* s, int lane) {
 
 // table slot `lane` (+ CPP, CXP) of the iteration the finalize will record
 struct CgsSlot {
-  double pz, cz, cpp, cxp;
+  double pz[CGS_SLOTS], cz[CGS_SLOTS], cpp, cxp;
 };
 __device__ inline CgsSlot cgs_slot_load(const CgsPre& p, const FinCtx& fc, int lane) {
-  CgsSlot o{0.0, 0.0, 1.0, 0.0};
+  CgsSlot o;
+#pragma unroll
+  for (int r = 0; r < CGS_SLOTS; ++r) o.pz[r] = o.cz[r] = 0.0;
+  o.cpp = 1.0;
+  o.cxp = 0.0;
   if (!fc.tab || fc.m <= 0) return o;
   const int i = p.iter + 1;
   const double* T = fc.tab + ((i / fc.m) & 1) * CGT;
-  o.pz = __ldcg(T + CG_PZ + lane);
-  o.cz = __ldcg(T + CG_CZ + lane);
+#pragma unroll
+  for (int r = 0; r < CGS_SLOTS; ++r) {
+    o.pz[r] = __ldcg(T + CG_PZ + lane + 32 * r);
+    o.cz[r] = __ldcg(T + CG_CZ + lane + 32 * r);
+  }
   o.cpp = __ldcg(T + CG_CPP);
   o.cxp = __ldcg(T + CG_CXP);
   return o;
@@ -386,20 +401,27 @@ __device__ inline void finalize_cgs_pre(const double* t, const CgsPre& p, const 
   }
   if (done || !fc.tab || fc.m <= 0) return;
   double* T = fc.tab + ((iter / fc.m) & 1) * CGT;
-  const int j = iter % fc.m, k = lane;
-  double pz = 0.0, cz = 0.0, cpp = 1.0, cxp = 0.0;
+  const int j = iter % fc.m;
+  double cpp = 1.0, cxp = 0.0;
   if (j != 0) {
-    pz = sl.pz;
-    cz = sl.cz;
     cpp = sl.cpp;
     cxp = sl.cxp;
   }
-  if (k < j) pz *= beta;
-  if (k == j) pz = 1.0;
-  if (k <= j) cz += alpha * pz;
-  T[CG_PZ + k] = pz;
-  T[CG_CZ + k] = cz;
-  if (k == 0) {
+#pragma unroll
+  for (int r = 0; r < CGS_SLOTS; ++r) {
+    const int k = lane + 32 * r;
+    double pz = 0.0, cz = 0.0;
+    if (j != 0) {
+      pz = sl.pz[r];
+      cz = sl.cz[r];
+    }
+    if (k < j) pz *= beta;
+    if (k == j) pz = 1.0;
+    if (k <= j) cz += alpha * pz;
+    T[CG_PZ + k] = pz;
+    T[CG_CZ + k] = cz;
+  }
+  if (lane == 0) {
     cpp *= beta;
     cxp += alpha * cpp;
     T[CG_CPP] = cpp;
@@ -486,7 +508,7 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
   __syncthreads();
   if (pre) CHB_TP(6);
   if (!am_last) return;
-  CgsSlot slot{0.0, 0.0, 1.0, 0.0};
+  CgsSlot slot;
   if (pre && wid == 0) slot = cgs_slot_load(*pre, ra.fc, lane);  // in flight with the partials
   // the last CTA sums the partials with all its warps (fixed partition and
   // order: deterministic), then one thread finalizes
