@@ -2,6 +2,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "comm.h"
@@ -30,7 +31,9 @@ struct NcclApi {
 NcclApi& api() {
   static NcclApi a;
   if (a.lib || a.ok) return a;
-  a.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  // CHB_NCCL_LIB: another NCCL build (or the tests' in-process loopback stand-in)
+  const char* path = getenv("CHB_NCCL_LIB");
+  a.lib = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!a.lib) return a;
 #define CHB_SYM(name) a.name = reinterpret_cast<decltype(a.name)>(dlsym(a.lib, "nccl" #name))
   CHB_SYM(GetUniqueId);
