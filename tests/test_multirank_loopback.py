@@ -34,13 +34,14 @@ def test_fake_transport_builds():
     assert os.path.exists(_build_fake())
 
 
-def _run_ranks(nx, ny, nranks, steps, **kw):
+def _run_ranks(nx, ny, nranks, steps, vslabs=1, **kw):
     import torch
     from paper_1811_11842_b200 import Simulation, unique_id
     from workloads import initial_fields
     uid = unique_id()
     out, its, errs = [None] * nranks, [None] * nranks, []
-    sims = [Simulation(nx, ny, rank=r, nranks=nranks, device=0, **kw) for r in range(nranks)]
+    sims = [Simulation(nx, ny, rank=r, nranks=nranks, device=0, virtual_slabs=vslabs, **kw)
+            for r in range(nranks)]
 
     def run(r):
         try:
@@ -72,14 +73,15 @@ def _run_ranks(nx, ny, nranks, steps, **kw):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nranks,solver", [(2, "bicgstab"), (3, "bicgstab"), (2, "gmres")])
-def test_multirank_loopback_matches_single_rank(nranks, solver, monkeypatch):
+@pytest.mark.parametrize("nranks,solver,vslabs", [(2, "bicgstab", 1), (3, "bicgstab", 1),
+                                                  (2, "gmres", 1), (2, "bicgstab", 2)])
+def test_multirank_loopback_matches_single_rank(nranks, solver, vslabs, monkeypatch):
     monkeypatch.setenv("CHB_NCCL_LIB", _build_fake())
     from paper_1811_11842_b200 import Simulation
     from workloads import initial_fields
     nx, ny = 40, 36
     kw = dict(Lambda=1e-5, rtol=1e-13, ch_solver=solver)
-    glob, its = _run_ranks(nx, ny, nranks, 2, **kw)
+    glob, its = _run_ranks(nx, ny, nranks, 2, vslabs=vslabs, **kw)
     sim = Simulation(nx, ny, **kw)
     sim.set_fields(**initial_fields(nx, ny, seed=4))
     sim.step(2)
