@@ -1,3 +1,7 @@
 mkdir -p gpurun_out
 S=gpurun_out/status.txt; : > $S
-timeout 900 python -m pytest tests/test_multirank_loopback.py -x -q > gpurun_out/loopback.log 2>&1; echo loopback=$? >> $S
+rm -f gpurun_out/kbench.jsonl
+for v in base h0 h20 h30 h40; do
+  if [ $v = base ]; then L=""; else L=$PWD/paper_1811_11842_b200/libch_b200_$v.so; fi
+  for op in poisson mom_v; do CHB_LIB=$L timeout 300 python scripts/kbench.py --solve $op | sed "s/^{/{\"lib\": \"$v\", /" >> gpurun_out/kbench.jsonl 2>> gpurun_out/kbench.err; echo $v$op=$? >> $S; done
+done
