@@ -1,7 +1,6 @@
 mkdir -p gpurun_out
 S=gpurun_out/status.txt; : > $S
-rm -f gpurun_out/kbench.jsonl
-for v in base h0 h20 h30 h40; do
-  if [ $v = base ]; then L=""; else L=$PWD/paper_1811_11842_b200/libch_b200_$v.so; fi
-  for op in poisson mom_v; do CHB_LIB=$L timeout 300 python scripts/kbench.py --solve $op | sed "s/^{/{\"lib\": \"$v\", /" >> gpurun_out/kbench.jsonl 2>> gpurun_out/kbench.err; echo $v$op=$? >> $S; done
+rm -f gpurun_out/slab.jsonl
+for ny in 4096 2048 1024 512; do
+  for op in poisson mom_v; do timeout 300 python scripts/kbench.py --solve $op --nx 4096 --ny $ny >> gpurun_out/slab.jsonl 2>> gpurun_out/slab.err; echo $ny$op=$? >> $S; done
 done
