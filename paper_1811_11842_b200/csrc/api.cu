@@ -561,7 +561,7 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
     // algorithmic bytes of the launch: K sweeps + the in-kernel p/x updates
     const long K = h->sch[sys].iter;
     if (!h->tm.pending.empty() && h->tm.pending.back().kc == kc_sys)
-      h->tm.pending.back().bytes = (cgs_bytes(kind, 0, 0) * (double)K +
+      h->tm.pending.back().bytes = (cgs_bytes(kind, 0, 1) * (double)K +
                                     8.0 * (m + 4) * (double)(K / m)) * cells;
   } else {
   const int tt = h->cg3 && NZ >= 3;
