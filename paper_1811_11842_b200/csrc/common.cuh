@@ -444,6 +444,13 @@ __device__ __forceinline__ void trace_put(int i, unsigned long long gt, unsigned
   chb_trace[blockIdx.x * 16 + i] = gt;
   chb_trace[blockIdx.x * 16 + 8 + i] = ck;
 }
+__device__ unsigned int chb_trace_smid[8192];
+__device__ __forceinline__ void trace_smid() {
+  if (threadIdx.x != 0) return;
+  unsigned int sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  chb_trace_smid[blockIdx.x] = sm;
+}
 __device__ __forceinline__ void trace_pt(int i) {
   unsigned long long gt, ck;
   trace_now(gt, ck);

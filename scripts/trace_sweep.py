@@ -31,14 +31,18 @@ g = torch.Generator(device="cuda").manual_seed(3)
 b = torch.randn((n, m), dtype=torch.float64, device="cuda", generator=g)
 if a.solve == "poisson":
     b -= b.mean()
-x = sim.solve(a.solve, b.cpu().numpy())
+if a.solve == "mom_v":
+    b[0] = 0.0  # the v wall row is not an unknown
+x = sim.solve(a.solve, b)
 path = "/tmp/chb_trace.bin"
 rc = _lib.lib.chb_trace_dump(path.encode(), a.nb)
 assert rc == 0, rc
 # points: 0 entry, 1 after griddepcontrol.wait, 2 ring ready, 3 row loop end,
 # 4 end (after the finalize in the last CTA), 5 reduction entry, 6 after the
 # ticket atomic, 7 last CTA: partial sums loaded and summed
-t = np.fromfile(path, dtype=np.uint64).reshape(a.nb, 16).astype(np.int64)
+raw = np.fromfile(path, dtype=np.uint8)
+t = raw[: a.nb * 128].view(np.uint64).reshape(a.nb, 16).astype(np.int64)
+smid = raw[a.nb * 128: a.nb * 132].view(np.uint32)
 gt, ck = t[:, :8], t[:, 8:]
 base = gt[:, 0].min()
 rel = (gt - base) / 1e3  # us
@@ -49,4 +53,18 @@ out = {"solve": a.solve, "config": cfg["name"], "nb": a.nb,
        "last_cta": last,
        "last_cta_gt_us": [round(float(v), 3) for v in rel[last]],
        "last_cta_cycles_from_p3": [int(v) for v in (ck[last] - ck[last, 3])]}
+# per-SM view: row-loop time (p3 - p2) of the CTAs on each SM
+loop = rel[:, 3] - rel[:, 2]
+per_sm = {}
+for b in range(a.nb):
+    per_sm.setdefault(int(smid[b]), []).append(float(loop[b]))
+sm_mean = np.array([np.mean(v) for v in per_sm.values()])
+within = np.mean([np.std(v) for v in per_sm.values()])
+out["loop_us"] = [round(float(loop.min()), 2), round(float(np.median(loop)), 2), round(float(loop.max()), 2)]
+out["per_sm"] = {"n_sm": len(per_sm), "ctas_per_sm": sorted({len(v) for v in per_sm.values()}),
+                 "sm_mean_loop_us": [round(float(sm_mean.min()), 2), round(float(np.median(sm_mean)), 2),
+                                     round(float(sm_mean.max()), 2)],
+                 "std_across_sm_means": round(float(sm_mean.std()), 2),
+                 "mean_std_within_sm": round(float(within), 2),
+                 "sm_means_by_smid": {str(k): round(float(np.mean(v)), 2) for k, v in sorted(per_sm.items())}}
 print(json.dumps(out))
