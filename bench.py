@@ -25,6 +25,7 @@ sys.path.insert(0, ROOT)
 from workloads import CONFIGS, initial_fields  # noqa: E402
 
 METRIC = "time-steps/s at 4096^2 fp64 (HBM roofline of the dominant stencil kernel reported)"
+METRIC_REF = "time-steps/s of the fp64 CPU oracle (whole steps at 256^2, BASELINE configs[1])"
 
 
 def _peaks():
@@ -84,66 +85,60 @@ class Clocks:
 
 
 # ------------------------------------------------------------- CPU oracle leg
-def oracle_step_estimate(nx: int, ny: int, iters: dict, seed: int = 0, n_iter: int = 6):
-    """Bounded sample of the oracle at the FULL grid: assemble the pressure
-    Poisson system and run `n_iter` of its textbook CG iterations, timed; a step
-    is then estimated as 5 assemblies + sum over the 5 systems of (iterations
-    of this workload) x (per-iteration time), BiCGStab iterations counted
-    twice (two matvecs).  Returns (seconds per step, sample description)."""
-    import numpy as np
+ORACLE_N = 256   # whole oracle steps are timed at BASELINE configs[1]'s grid (2-3 s each)
+
+
+def oracle_whole_steps(n_steps: int, n: int = ORACLE_N, seed: int = 0, warm: int = 0):
+    """Time `n_steps` WHOLE oracle time steps (assembly + every Krylov solve of
+    the step, §4) at n x n from the seeded BASELINE initial condition,
+    after `warm` untimed ones.  Returns (seconds per step, Krylov iterations
+    per step, cores used)."""
     import oracle  # noqa: F401  (sets single-threaded BLAS)
-    from oracle import assemble as asm, explicit as ex
-    from oracle.krylov import NotConverged, cg
-    f = initial_fields(nx, ny, seed=seed)
+    from oracle import Params, initial_state, step
+    st = initial_state(initial_fields(n, n, seed=seed))
+    prm = Params()
+    for _ in range(warm):
+        st, _ = step(st, prm)
+    its = {}
     t0 = time.perf_counter()
-    bx, by = ex.pressure_faces(f["phi"], 1.0, 1.0)
-    A = asm.poisson_matrix(nx, ny, bx, by)
-    b = np.random.default_rng(0).standard_normal(nx * ny)
-    t_asm = time.perf_counter() - t0
-    t1 = time.perf_counter()
-    try:
-        cg(A, b, np.zeros(nx * ny), 1.0 / A.diagonal(), 1e-30, n_iter, nullspace=True)
-    except NotConverged:
-        pass
-    t_it = (time.perf_counter() - t1) / n_iter
-    total_it = sum(v * (2 if k == "ch" else 1) for k, v in iters.items())
-    est = 5 * t_asm + total_it * t_it
-    sample = (f"oracle at {nx}x{ny}: pressure-system assembly ({t_asm:.2f}s) + {n_iter} CG "
-              f"iterations ({t_it:.3f}s each) timed; step = 5 assemblies + {total_it} "
-              f"iterations (this workload's per-step Krylov counts)")
-    return est, sample, t_asm + n_iter * t_it
+    for _ in range(n_steps):
+        st, info = step(st, prm)
+        for k, v in info.iters.items():
+            its[k] = its.get(k, 0) + v
+    sec = (time.perf_counter() - t0) / n_steps
+    return sec, {k: v / n_steps for k, v in its.items()}, 1
 
 
-def _iters_table(cfg_idx):
-    p = os.path.join(ROOT, "profiles", f"iters_config{cfg_idx}.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            return json.load(f)
-    return None
+def estimate_full_size(sec_small, iters_small, iters_full, n_small, n_full):
+    """Labelled extrapolation (NOT a measurement): the oracle's cost per Krylov
+    iteration scales with the cell count; a step at n_full costs the measured
+    small step x (cells ratio) x (Krylov iterations ratio)."""
+    cells = (n_full / n_small) ** 2
+    its_s = sum(v * (2 if k == "ch" else 1) for k, v in iters_small.items())
+    its_f = sum(v * (2 if k == "ch" else 1) for k, v in iters_full.items())
+    return sec_small * cells * (its_f / max(its_s, 1))
 
 
 def run_reference(args, rank, world):
     """--impl reference: the oracle (there is no reference implementation),
-    timed on the host cores, each step a bounded sample of the workload."""
+    timed on the host cores as WHOLE time steps of BASELINE configs[1]'s 256^2
+    grid (the largest configured grid whose steps fit the driver's clock;
+    4096^2 is ~5 h per step on one core).  A 4096^2 figure is reported only as
+    a separately labelled extrapolation."""
     if rank != 0:
         return 0
-    cfg = CONFIGS[args.config]
-    nx, ny = cfg["nx"], cfg["ny"]
-    iters = _iters_table(args.config) or {"ch": 2, "nutrient": 400, "u": 14000, "v": 14000, "p": 16000}
-    ests = []
-    sample = ""
-    for k in range(args.warmup + args.steps):
-        est, sample, _ = oracle_step_estimate(nx, ny, iters, n_iter=3)
-        if k >= args.warmup:
-            ests.append(est)
-    sec = sum(ests) / len(ests)
+    sec, its, cores = oracle_whole_steps(args.steps, warm=args.warmup)
     v = 1.0 / sec
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "time-steps/s",
+    line = {"impl": "reference", "metric": METRIC_REF, "value": v, "unit": "time-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": cfg["name"], "nx": nx, "ny": ny},
-            "cpu_baseline": {"value": v, "unit": "time-steps/s", "cores": 1, "kind": "oracle",
-                             "sample": sample},
+            "data": "synthetic",
+            "config": {"workload": CONFIGS[1]["name"], "nx": ORACLE_N, "ny": ORACLE_N,
+                       "dt": CONFIGS[1]["dt"], "krylov_iters_per_step": its},
+            "cell_steps_per_s": v * ORACLE_N * ORACLE_N,
+            "cpu_baseline": {"value": v, "unit": "time-steps/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} whole oracle steps at {ORACLE_N}^2 after "
+                                       f"{args.warmup} untimed ({CONFIGS[1]['name']})"},
             "e2e": {"value": v, "unit": "time-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -249,9 +244,16 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        est, sample, wall = oracle_step_estimate(nx, ny, {k: int(round(v)) for k, v in iters_step.items()})
-        cpu = {"value": 1.0 / est, "unit": "time-steps/s", "cores": 1, "kind": "oracle",
-               "sample": sample, "sample_wall_s": round(wall, 2)}
+        csec, cits, cores = oracle_whole_steps(args.cpu_steps)
+        est = estimate_full_size(csec, cits, iters_step, ORACLE_N, nx)
+        cpu = {"value": 1.0 / csec, "unit": "time-steps/s", "cores": cores, "kind": "oracle",
+               "sample": f"{args.cpu_steps} whole oracle steps at {ORACLE_N}^2 "
+                         f"({CONFIGS[1]['name']}, seeded initial condition)",
+               "sample_wall_s": round(csec * args.cpu_steps, 2),
+               "cell_steps_per_s": ORACLE_N * ORACLE_N / csec,
+               "estimate": {"value": 1.0 / est, "unit": f"time-steps/s at {nx}^2",
+                            "how": "extrapolated, not measured: measured 256^2 step x cells "
+                                   "ratio x Krylov-iteration ratio"}}
 
     if rank == 0:
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
@@ -259,11 +261,14 @@ def run_ours(args, rank, world, local_rank):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": cfg["name"], "nx": nx, "ny": ny, "dt": cfg["dt"],
+                "config": {"workload": cfg["name"] if args.steps == cfg["steps"] else
+                           f"{nx}x{ny}_{args.steps}steps (declared: {cfg['steps']})",
+                           "nx": nx, "ny": ny, "dt": cfg["dt"],
                            "parallelism": f"slab-y x{world}", "ch_solver": args.ch_solver,
                            "rtol": sp.rtol, "true_residual_refine": sp.refine,
                            "l2": "inputs larger than L2 (134 MB per field)",
                            "krylov_iters_per_step": iters_step},
+                "cell_steps_per_s": value * nx * ny,
                 "roofline": roof, "kernels": per_class, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": st["launches"] * world, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
@@ -273,11 +278,13 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: the configuration's step count, 20 for configs[3])")
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--cpu-steps", type=int, default=5, help="whole oracle steps of cpu_baseline")
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -288,7 +295,14 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
+    if args.steps is None:
+        args.steps = CONFIGS[args.config]["steps"]
+    return args
+
+
+def main():
+    args = parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))

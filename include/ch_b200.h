@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define CH_ABI_VERSION 1
+#define CH_ABI_VERSION 2
 
 enum {
   CH_OK = 0,
@@ -70,9 +70,9 @@ enum { CH_SYS_CH = 0, CH_SYS_NUTRIENT = 1, CH_SYS_U = 2, CH_SYS_V = 3, CH_SYS_P 
 
 /* Operators for ch_apply_operator (isolated matrix-free stencil sweeps). */
 enum {
-  CH_OP_CH = 0,       /* y = [I/dt + (G1/2) L_{M*} Delta_h] x, M* from the current phi, phi_prev  */
+  CH_OP_CH = 0,       /* y = [I/dt + th G1 L_{M*} Delta_h + ta Adv(.; v^n)] x, M* from phi, phi_prev */
   CH_OP_POISSON = 1,  /* y = -D_h beta G_h x, beta = 1/rho(current phi) on faces (Eq. 20 LHS)      */
-  CH_OP_MOM_U = 2,    /* y = [a - 1/2 Delta_h^0] x on x-faces, a = 1/(nu(phi*) dt)                 */
+  CH_OP_MOM_U = 2,    /* y = [a - theta_visc Delta_h^0] x on x-faces, a = 1/(nu(phi*) dt)          */
   CH_OP_MOM_V = 3     /* same on y-faces, wall row identity                                       */
 };
 
@@ -80,7 +80,7 @@ enum {
 enum { CH_SOLVER_BICGSTAB = 0, CH_SOLVER_GMRES = 1 };
 
 typedef struct ch_grid {
-  int32_t nx, ny;        /* global cells; nx >= 4, ny >= 4                              */
+  int32_t nx, ny;        /* global cells; nx even and >= 4, ny >= 4                     */
   int32_t rank, nranks;  /* slab decomposition in y over processes (1 GPU each)          */
   int32_t device;        /* CUDA device ordinal for this handle                          */
   int32_t virtual_slabs; /* >= 1: split this rank's rows into that many slabs with halo   */
@@ -105,6 +105,12 @@ typedef struct ch_params {
   double rho_s;    /* rho_s / rho_0                  (1)           */
   double lid_u;    /* top-wall tangential velocity U0 (1, R10)     */
   double rtol;     /* Krylov relative residual ||r||/||b|| (1e-10) */
+  /* Implicit weights of the time discretisation (R5, R7, R12, R23). */
+  double theta_ch;   /* Gamma1 fourth-order CH term: 0.5 = Crank-Nicolson       */
+                     /* ("Crank-Nicholson ... in R and f"), [0,1]  */
+  double theta_adv;  /* advection div(phi v^n) in the CH system: 0.5 = CN, [0,1] */
+  double theta_visc; /* viscous term of Eq. 19: 1 = at u^{n+1} (the BVP "for    */
+                     /* u^{n+1}"), (0,1]                       */
   int32_t maxit;   /* iteration cap per solve                      */
   int32_t ch_solver;      /* CH_SOLVER_*                           */
   int32_t gmres_restart;  /* m of GMRES(m), 1..64                  */
@@ -112,6 +118,8 @@ typedef struct ch_params {
                    /* from the converged x until the TRUE residual   */
                    /* ||b - A x|| <= rtol ||b|| (0 = stop on the     */
                    /* method's recursive residual, PETSc's default)  */
+  int32_t startup_be; /* steps with time index n < startup_be take theta_ch =  */
+                      /* theta_adv = 1 (backward-Euler start-up, R23), >= 0    */
 } ch_params;
 
 typedef struct ch_stats {
@@ -175,6 +183,12 @@ int ch_partition(int32_t ny, int32_t nranks, int32_t rank, int32_t virtual_slabs
 /* Use `stream` (a cudaStream_t, may be NULL = legacy default) for all work. */
 int ch_set_stream(ch_handle* h, void* stream);
 
+/* Time index n of the state (0 after ch_create; +1 per completed step).  It
+ * selects the backward-Euler start-up steps (params.startup_be, R23); a caller
+ * restoring a saved state sets it back with ch_set_time_index.  n >= 0. */
+int ch_set_time_index(ch_handle* h, int64_t n);
+int ch_get_time_index(const ch_handle* h, int64_t* n);
+
 /* Set the state (any pointer may be NULL = leave unchanged).  Each array is
  * the local slab, nrows x nx, ld = nx.  Setting phi also sets phi_prev = phi
  * (first step extrapolates to phi* = phi^0, R5). */
@@ -185,8 +199,8 @@ int ch_set_field(ch_handle* h, int field, const double* src, int where);
 /* Advance nsteps time steps of the semi-implicit scheme (§4, lines
  * 117-151; splitting order DESIGN.md R1), each step:
  *   1. phi* = (3 phi^n - phi^{n-1}) / 2; Cahn-Hilliard system (Eq. 16 4th
- *      line with Eq. 4-5, Crank-Nicolson on the Gamma1 term) solved by
- *      BiCGStab / GMRES(m) with Jacobi;
+ *      line with Eq. 4-5; theta-weighted Gamma1 term and advection, CN by
+ *      default) solved by BiCGStab / GMRES(m) with Jacobi;
  *   2. nutrient c^{n+1} (Eq. 16 3rd line, Eq. 7), Jacobi-PCG;
  *   3. intermediate velocity u*, v* (Eq. 18-19, R6-R7), Jacobi-PCG each;
  *   4. pressure -div(1/rho grad p) = div u* (Eq. 20) with the constant null

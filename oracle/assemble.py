@@ -130,13 +130,36 @@ def mac_grad(nx, ny):
                          shape=(2 * n, n))
 
 
-def ch_matrix(nx, ny, dt, Gamma1, Mx, My):
+def advection_matrix(nx, ny, u, v):
+    """Conservative central advection s -> div_h(s v) on the MAC grid (Eq. 16
+    "∇·(φ_n v)", central differences §4; R12) as a matrix, for
+    the implicit (Crank-Nicolson) part of the CH step (R12).  Face values of s
+    are arithmetic means; v = 0 on the wall faces (Eq. 22, v·n = 0)."""
+    hx, hy = 1.0 / nx, 1.0 / ny
+    uW = np.asarray(u, dtype=np.float64)
+    uE = np.roll(uW, -1, axis=1)               # u on the right face of cell i
+    vS = np.array(v, dtype=np.float64, copy=True)
+    vS[0] = 0.0                                 # bottom wall face
+    vN = np.zeros_like(vS)
+    vN[:-1] = vS[1:]                            # top face of row j (wall at j = ny-1)
+    ent = [(1, 0, uE / (2 * hx)), (-1, 0, -uW / (2 * hx)),
+           (0, 1, vN / (2 * hy)), (0, -1, -vS / (2 * hy)),
+           (0, 0, (uE - uW) / (2 * hx) + (vN - vS) / (2 * hy))]
+    return stencil_matrix(nx, ny, ent, "mirror")
+
+
+def ch_matrix(nx, ny, dt, Gamma1, Mx, My, theta=0.5, theta_adv=0.0, u=None, v=None):
     """Implicit Cahn-Hilliard operator (Eq. 16 4th line with §4's
-    Crank-Nicolson, R5):  A = I/dt + (Gamma1/2) L_M Delta_h.
-    Nonsymmetric (product of two different symmetric operators), 13-point."""
+    Crank-Nicolson, R5, R12):
+        A = I/dt + theta Gamma1 L_M Delta_h + theta_adv Adv(.; v^n).
+    Nonsymmetric (product of two different symmetric operators, plus the
+    skew advection part), 13-point."""
     n = nx * ny
-    return (sp.identity(n, format="csr") / dt
-            + (0.5 * Gamma1) * (flux_div(nx, ny, Mx, My) @ lap(nx, ny, "mirror"))).tocsr()
+    A = (sp.identity(n, format="csr") / dt
+         + (theta * Gamma1) * (flux_div(nx, ny, Mx, My) @ lap(nx, ny, "mirror")))
+    if theta_adv != 0.0:
+        A = A + theta_adv * advection_matrix(nx, ny, u, v)
+    return A.tocsr()
 
 
 def nutrient_matrix(nx, ny, a_c, Kx, Ky):
@@ -144,17 +167,33 @@ def nutrient_matrix(nx, ny, a_c, Kx, Ky):
     return (sp.diags(np.ravel(a_c)) - 0.5 * flux_div(nx, ny, Kx, Ky)).tocsr()
 
 
-def u_matrix(nx, ny, a_u):
-    """Scaled Crank-Nicolson viscous operator for u (Eq. 19, R6-R7):
-    diag(a_u) - (1/2) Delta_h^{u,0}, a_u = 1/(nu dt).  SPD."""
-    return (sp.diags(np.ravel(a_u)) - 0.5 * lap(nx, ny, "odd")).tocsr()
+def node_flux_div(nx, ny, KW, KE, KS, KN, kind):
+    """div_h(K grad_h .) of one velocity component from its four face
+    coefficient arrays (explicit.node_fluxes), ghost rule `kind` ("odd": u,
+    "vface": v; rows j >= 1 only, row 0 all zero)."""
+    hx2, hy2 = (1.0 / nx) ** 2, (1.0 / ny) ** 2
+    ent = [(1, 0, KE / hx2), (-1, 0, KW / hx2), (0, 1, KN / hy2), (0, -1, KS / hy2),
+           (0, 0, -(KE + KW) / hx2 - (KN + KS) / hy2)]
+    A = stencil_matrix(nx, ny, ent, kind)
+    if kind == "vface":
+        interior = np.ones(nx * ny)
+        interior[:nx] = 0.0
+        A = sp.diags(interior) @ A
+    return A.tocsr()
 
 
-def v_matrix(nx, ny, a_v):
+def u_matrix(nx, ny, a_u, K, theta=1.0):
+    """Implicit viscous operator for u (Eq. 19, R6-R7): diag(a_u) - theta div_h(eta grad_h),
+    a_u = rho/dt, K = (KW, KE, KS, KN) face coefficients of eta (theta = 1: the
+    boundary value problem for u^{n+1} as printed; 1/2: Crank-Nicolson).  SPD."""
+    return (sp.diags(np.ravel(a_u)) - theta * node_flux_div(nx, ny, *K, "odd")).tocsr()
+
+
+def v_matrix(nx, ny, a_v, K, theta=1.0):
     """Same for v on interior y-faces; the wall row j = 0 is an identity row."""
     a = np.array(a_v, dtype=np.float64, copy=True)
     a[0, :] = 1.0
-    return (sp.diags(np.ravel(a)) - 0.5 * lap(nx, ny, "vface")).tocsr()
+    return (sp.diags(np.ravel(a)) - theta * node_flux_div(nx, ny, *K, "vface")).tocsr()
 
 
 def poisson_matrix(nx, ny, beta_x, beta_y):

@@ -84,10 +84,13 @@ def face_from_cells(w, scale=1.0, clip=False):
     return k
 
 
-def ch_apply(phis, x, dt, Gamma1, Lambda):
-    """x/dt + (G1/2) div(Lambda phi* grad(Delta x))  (R5)."""
+def ch_apply(phis, x, dt, Gamma1, Lambda, theta=0.5, theta_adv=0.0, u=None, v=None):
+    """x/dt + theta G1 div(Lambda phi* grad(Delta x)) + theta_adv div(x v)  (R5, R12)."""
     w = lap(x)
-    return x / dt + 0.5 * Gamma1 * flux_div(face_from_cells(phis, Lambda, clip=True), w)
+    out = x / dt + theta * Gamma1 * flux_div(face_from_cells(phis, Lambda, clip=True), w)
+    if theta_adv != 0.0:
+        out = out + theta_adv * advection(x, u, v)
+    return out
 
 
 def poisson_apply(phi1, p, rho_n, rho_s):
@@ -101,21 +104,29 @@ def poisson_apply(phi1, p, rho_n, rho_s):
     return -flux_div(k, p)
 
 
-def u_apply(a_u, x):
-    """a x - 1/2 Delta^0 x for u (odd reflection, homogeneous)."""
+def _kmean(w, ja, ia, jb, ib):
+    """Mean of a node coefficient at two unknown points (mirror rows, periodic x)."""
+    return 0.5 * (S(w, ja, ia) + S(w, jb, ib))
+
+
+def u_apply(a_u, eta, x, theta=1.0):
+    """a x - theta div(eta grad x) for u (odd reflection, homogeneous), face
+    coefficient = mean of eta at the two u points."""
     ny, nx = x.shape
     out = np.zeros_like(x)
     for j in range(ny):
         for i in range(nx):
             c = U(x, j, i, 0.0)
-            lapx = ((U(x, j, i + 1, 0.0) - 2 * c + U(x, j, i - 1, 0.0)) * nx * nx
-                    + (U(x, j + 1, i, 0.0) - 2 * c + U(x, j - 1, i, 0.0)) * ny * ny)
-            out[j, i] = a_u[j, i] * c - 0.5 * lapx
+            fe = _kmean(eta, j, i, j, i + 1) * (U(x, j, i + 1, 0.0) - c)
+            fw = _kmean(eta, j, i - 1, j, i) * (c - U(x, j, i - 1, 0.0))
+            fn = _kmean(eta, j, i, j + 1, i) * (U(x, j + 1, i, 0.0) - c)
+            fs = _kmean(eta, j - 1, i, j, i) * (c - U(x, j - 1, i, 0.0))
+            out[j, i] = a_u[j, i] * c - theta * ((fe - fw) * nx * nx + (fn - fs) * ny * ny)
     return out
 
 
-def v_apply(a_v, x):
-    """a x - 1/2 Delta^0 x on interior y-faces, identity on the wall row."""
+def v_apply(a_v, eta, x, theta=1.0):
+    """a x - theta div(eta grad x) on interior y-faces, identity on the wall row."""
     ny, nx = x.shape
     out = np.zeros_like(x)
     for i in range(nx):
@@ -123,10 +134,47 @@ def v_apply(a_v, x):
     for j in range(1, ny):
         for i in range(nx):
             c = V(x, j, i)
-            lapx = ((V(x, j, i + 1) - 2 * c + V(x, j, i - 1)) * nx * nx
-                    + (V(x, j + 1, i) - 2 * c + V(x, j - 1, i)) * ny * ny)
-            out[j, i] = a_v[j, i] * c - 0.5 * lapx
+            fe = _kmean(eta, j, i, j, i + 1) * (V(x, j, i + 1) - c)
+            fw = _kmean(eta, j, i - 1, j, i) * (c - V(x, j, i - 1))
+            fn = _kmean(eta, j, i, j + 1, i) * (V(x, j + 1, i) - c)
+            fs = _kmean(eta, j - 1, i, j, i) * (c - V(x, j - 1, i))
+            out[j, i] = a_v[j, i] * c - theta * ((fe - fw) * nx * nx + (fn - fs) * ny * ny)
     return out
+
+
+def visc_transpose(u, v, phis, Re_n, Re_s):
+    """div(eta (grad v)^T) on the MAC faces, eta(phi) = f/Re_n + (1-f)/Re_s,
+    f = clip(phi, 0, 1), at cell centres and at corners (phi = mean of the
+    four cells, mirror rows)."""
+    ny, nx = u.shape
+
+    def eta(p):
+        f = min(max(p, 0.0), 1.0)
+        return f / Re_n + (1.0 - f) / Re_s
+
+    eta_cell = np.array([[eta(phis[j, i]) for i in range(nx)] for j in range(ny)])
+
+    def ek(j, i):  # corner (i hx, j hy)
+        return eta(0.25 * (S(phis, j, i) + S(phis, j, i - 1) + S(phis, j - 1, i)
+                           + S(phis, j - 1, i - 1)))
+
+    tx = np.zeros_like(u)
+    ty = np.zeros_like(v)
+    for j in range(ny):
+        for i in range(nx):
+            qe = S(eta_cell, j, i) * (U(u, j, i + 1, 0.0) - U(u, j, i, 0.0)) * nx
+            qw = S(eta_cell, j, i - 1) * (U(u, j, i, 0.0) - U(u, j, i - 1, 0.0)) * nx
+            rn = ek(j + 1, i) * (V(v, j + 1, i) - V(v, j + 1, i - 1)) * nx
+            rs = ek(j, i) * (V(v, j, i) - V(v, j, i - 1)) * nx
+            tx[j, i] = (qe - qw) * nx + (rn - rs) * ny
+    for j in range(1, ny):
+        for i in range(nx):
+            qe = ek(j, i + 1) * (U(u, j, i + 1, 0.0) - U(u, j - 1, i + 1, 0.0)) * ny
+            qw = ek(j, i) * (U(u, j, i, 0.0) - U(u, j - 1, i, 0.0)) * ny
+            rn = S(eta_cell, j, i) * (V(v, j + 1, i) - V(v, j, i)) * ny
+            rs = S(eta_cell, j - 1, i) * (V(v, j, i) - V(v, j - 1, i)) * ny
+            ty[j, i] = (qe - qw) * nx + (rn - rs) * ny
+    return tx, ty
 
 
 def divergence(u, v):
@@ -207,7 +255,7 @@ def lap_at(s, j, i):
             + (S(s, j + 1, i) - 2 * c + S(s, j - 1, i)) * ny * ny)
 
 
-def ch_apply_at(phis, x, j, i, dt, Gamma1, Lambda):
+def ch_apply_at(phis, x, j, i, dt, Gamma1, Lambda, theta=0.5, theta_adv=0.0, u=None, v=None):
     ny, nx = x.shape
 
     def m(ja, ia, jb, ib):
@@ -218,7 +266,15 @@ def ch_apply_at(phis, x, j, i, dt, Gamma1, Lambda):
     fw = m(j, i - 1, j, i) * (wc - lap_at(x, j, i - 1))
     fn = m(j, i, j + 1, i) * (lap_at(x, j + 1, i) - wc) if j + 1 < ny else 0.0
     fs = m(j - 1, i, j, i) * (wc - lap_at(x, j - 1, i)) if j > 0 else 0.0
-    return S(x, j, i) / dt + 0.5 * Gamma1 * ((fe - fw) * nx * nx + (fn - fs) * ny * ny)
+    out = S(x, j, i) / dt + theta * Gamma1 * ((fe - fw) * nx * nx + (fn - fs) * ny * ny)
+    if theta_adv != 0.0:
+        c = S(x, j, i)
+        ae = U(u, j, i + 1, 0.0) * 0.5 * (c + S(x, j, i + 1))
+        aw = U(u, j, i, 0.0) * 0.5 * (c + S(x, j, i - 1))
+        an = V(v, j + 1, i) * 0.5 * (c + S(x, j + 1, i))
+        as_ = V(v, j, i) * 0.5 * (c + S(x, j - 1, i))
+        out += theta_adv * ((ae - aw) * nx + (an - as_) * ny)
+    return out
 
 
 def poisson_at(phi1, p, j, i, rho_n, rho_s):

@@ -73,9 +73,18 @@ def advection(s, u, v):
     return (uE * sE - u * sW) / hx + (vN * sN - vS * sS) / hy
 
 
+def volume_fraction(phi):
+    """The physical volume fraction clip(phi, 0, 1) at which the material laws
+    and rates of phi_n are evaluated ("volume fraction",
+    PAPER.md:42 phi_n + phi_s = 1; R24).  The discrete phi leaves [0, 1] by
+    the dispersive ripples of the central scheme."""
+    return np.clip(phi, 0.0, 1.0)
+
+
 def growth(phis, c, eps, mu, Kc):
-    """g_n = eps mu phi_n c/(K_c + c) (Eq. 5; "c'" read as c, R8)."""
-    return eps * mu * phis * c / (Kc + c)
+    """g_n = eps mu phi_n c/(K_c + c) (Eq. 5; "c'" read as c, R8),
+    phi_n the volume fraction (R24)."""
+    return eps * mu * volume_fraction(phis) * c / (Kc + c)
 
 
 # ------------------------------------------------------------ momentum pieces
@@ -93,14 +102,19 @@ def face_phi_v(phis):
 
 
 def density(phi, rho_n, rho_s):
-    """rho~ = phi_s rho_s/rho0 + phi_n rho_n/rho0 (Eq. 15)."""
-    return rho_s + phi * (rho_n - rho_s)
+    """rho~ = phi_s rho_s/rho0 + phi_n rho_n/rho0 (Eq. 15), at the
+    volume fraction clip(phi, 0, 1) (R24)."""
+    f = volume_fraction(phi)
+    return rho_s + f * (rho_n - rho_s)
 
 
 def inv_reynolds(phi, Re_n, Re_s):
     """1/Re_a = phi_n/Re_n + phi_s/Re_s, the volume-fraction average that makes
-    phi_n tau_n + phi_s tau_s = (2/Re_a) D (Eq. 8, Eq. 17; R6)."""
-    return phi / Re_n + (1.0 - phi) / Re_s
+    phi_n tau_n + phi_s tau_s = (2/Re_a) D (Eq. 8, Eq. 17; R6), at the volume
+    fraction clip(phi, 0, 1) (R24: with Re_n/Re_s = 2.3e-6 any phi below
+    -2.3e-6 would make the mixture viscosity negative)."""
+    f = volume_fraction(phi)
+    return f / Re_n + (1.0 - f) / Re_s
 
 
 def convective_u(u, v, lid_u):
@@ -157,22 +171,76 @@ def phase_stress(phis, Gamma1):
     return Rx, Ry
 
 
-def lap_u_inhom(u, lid_u):
-    """Delta_h u with the no-slip / lid ghosts (inhomogeneous)."""
+def viscosity_u(phis, Re_n, Re_s):
+    """eta = 1/Re_a (R6, R24) at the u points (x-faces), from the face mean of phi*."""
+    return inv_reynolds(face_phi_u(phis), Re_n, Re_s)
+
+
+def viscosity_v(phis, Re_n, Re_s):
+    """eta at the v points (y-faces j >= 1; row 0, the wall, from phi[0])."""
+    return inv_reynolds(face_phi_v(phis), Re_n, Re_s)
+
+
+def node_fluxes(w):
+    """Face coefficients of div(w grad .) between adjacent unknown points of one
+    velocity component, K = arithmetic mean of w at the two points (R6): returns
+    (KW, KE, KS, KN), KW[j, i] between points (j, i-1) and (j, i), KS[j, i]
+    between (j-1, i) and (j, i); the coefficient's wall ghost is its mirror
+    image (KS[0] = w[0], KN[ny-1] = w[ny-1])."""
+    KW = 0.5 * (np.roll(w, 1, axis=1) + w)
+    KE = np.roll(KW, -1, axis=1)
+    wp = np.vstack([w[:1], w, w[-1:]])
+    KS = 0.5 * (wp[:-2] + wp[1:-1])
+    KN = 0.5 * (wp[2:] + wp[1:-1])
+    return KW, KE, KS, KN
+
+
+def visc_u_inhom(u, eta_u, lid_u):
+    """div_h(eta grad_h u) at the u points with the no-slip / lid ghosts
+    (inhomogeneous; the viscous term of Eq. 18-19 in conservative form, R6)."""
     ny, nx = u.shape
     up = pad_u(u, lid_u)
-    return ((up[1:-1, 2:] - 2 * u + up[1:-1, :-2]) * nx * nx
-            + (up[2:, 1:-1] - 2 * u + up[:-2, 1:-1]) * ny * ny)
+    KW, KE, KS, KN = node_fluxes(eta_u)
+    return ((KE * (up[1:-1, 2:] - u) - KW * (u - up[1:-1, :-2])) * nx * nx
+            + (KN * (up[2:, 1:-1] - u) - KS * (u - up[:-2, 1:-1])) * ny * ny)
 
 
-def lap_v(v):
-    """Delta_h v on interior y-faces with v = 0 on both walls; row 0 -> 0."""
+def visc_v(v, eta_v):
+    """div_h(eta grad_h v) on interior y-faces with v = 0 on both walls; row 0 -> 0."""
     ny, nx = v.shape
     vp = pad_v(v)
-    out = ((vp[1:-1, 2:] - 2 * v + vp[1:-1, :-2]) * nx * nx
-           + (vp[2:, 1:-1] - 2 * v + vp[:-2, 1:-1]) * ny * ny)
+    KW, KE, KS, KN = node_fluxes(eta_v)
+    out = ((KE * (vp[1:-1, 2:] - v) - KW * (v - vp[1:-1, :-2])) * nx * nx
+           + (KN * (vp[2:, 1:-1] - v) - KS * (v - vp[:-2, 1:-1])) * ny * ny)
     out[0] = 0.0
     return out
+
+
+def visc_transpose(u, v, phis, Re_n, Re_s):
+    """The rest of the viscous stress, div(eta (grad v)^T), so that with the
+    implicit div(eta grad v) the momentum equation carries div(2 eta D) =
+    div(phi_n tau_n + phi_s tau_s) (Eq. 8-9, 15; R6: Eq. 17's viscous part of
+    R).  MAC discretisation: eta at cell centres (d u/dx, d v/dy there) and at
+    corners (mean of the four cells, mirror rows; d v/dx, d u/dy there).
+    Returns (T_x on x-faces, T_y on y-faces with row 0 = 0)."""
+    ny, nx = u.shape
+    hx, hy = 1.0 / nx, 1.0 / ny
+    ec = inv_reynolds(phis, Re_n, Re_s)
+    p = np.pad(phis, ((1, 1), (0, 0)), mode="symmetric")
+    pk = 0.25 * (p[1:] + np.roll(p[1:], 1, axis=1) + p[:-1] + np.roll(p[:-1], 1, axis=1))
+    ek = inv_reynolds(pk, Re_n, Re_s)                   # corners (i hx, j hy), j = 0..ny
+    vf = np.vstack([v, np.zeros((1, nx))])               # v[ny] = 0 (top wall)
+    vf[0] = 0.0                                          # bottom wall
+    qc = ec * (np.roll(u, -1, axis=1) - u) / hx          # eta du/dx at cells
+    dvdx = (vf - np.roll(vf, 1, axis=1)) / hx            # dv/dx at corners
+    Tx = (qc - np.roll(qc, 1, axis=1)) / hx + (ek[1:] * dvdx[1:] - ek[:-1] * dvdx[:-1]) / hy
+    dudy = np.zeros((ny + 1, nx))
+    dudy[1:ny] = (u[1:] - u[:-1]) / hy                   # du/dy at interior corners
+    qk = ek * dudy
+    rc = ec * (vf[1:] - vf[:-1]) / hy                    # eta dv/dy at cells
+    Ty = np.zeros_like(v)
+    Ty[1:] = (np.roll(qk, -1, axis=1) - qk)[1:ny] / hx + (rc[1:] - rc[:-1]) / hy
+    return Tx, Ty
 
 
 # ----------------------------------------------------------- projection pieces

@@ -7,6 +7,17 @@ epsilon (Eq. 5, "a scaling constant", no value printed) defaults to 1 [R8].
 rho_n/rho_0 = rho_s/rho_0 = 1 (Table 1 lists both densities as 1e3) [R9].
 lid_u: top-wall tangential velocity; BASELINE.json reads "u = y at the top
 wall", i.e. u(x, 1) = 1 [R10]; the paper's §5.1 run used 0.1 (Eq. 22).
+
+Time discretisation (implicit weights, R5, R7, R12, R23):
+  theta_ch   Gamma1 fourth-order part of the CH equation: 1/2 = Crank-Nicolson
+             ("Crank-Nicholson and extrapolation for the non-linear terms in R
+             and f", PAPER.md:142);
+  theta_adv  advection div(phi_n v^n) inside the CH system: 1/2 = Crank-Nicolson;
+  theta_visc viscous term of Eq. 19: 1 = implicit at u^{n+1}, the boundary value
+             problem "for u^{n+1}" with boundary values of u^{n+1} (PAPER.md:128-132);
+  startup_be the first `startup_be` steps (time index n < startup_be) take
+             theta_ch = theta_adv = 1 (backward-Euler start-up of the CN scheme
+             for the discontinuous initial phi of BASELINE.json, R23).
 """
 from __future__ import annotations
 
@@ -29,6 +40,10 @@ class Params:
     rho_n: float = 1.0
     rho_s: float = 1.0
     lid_u: float = 1.0
+    theta_ch: float = 0.5
+    theta_adv: float = 0.5
+    theta_visc: float = 1.0
+    startup_be: int = 2
     rtol: float = 1e-10
     maxit: int = 200000
     ch_solver: str = "bicgstab"   # "bicgstab" | "gmres"   [R14]

@@ -50,20 +50,30 @@ def _solve_ch(A, b, x0, dinv, prm: Params):
     return bicgstab(A, b, x0, dinv, prm.rtol, prm.maxit)
 
 
+def ch_thetas(st: State, prm: Params):
+    """Implicit weights of the step at time index st.n: the CN weights, or 1
+    during the backward-Euler start-up steps (R23)."""
+    if st.n < prm.startup_be:
+        return 1.0, 1.0
+    return prm.theta_ch, prm.theta_adv
+
+
 def ch_system(st: State, prm: Params):
-    """Linear system of the CH step (Eq. 16 4th line, Eq. 4-5; R5):
-      [I/dt + (G1/2) L_{M*} Δ_h] phi^{n+1}
-        = phi^n/dt + L_{M*}( F'(phi*) - (G1/2) Δ_h phi^n ) - div_h(phi* v^n) + g_n(phi*, c^n)
-    Returns (A, b, phi*)."""
+    """Linear system of the CH step (Eq. 16 4th line, Eq. 4-5; R5, R12):
+      [I/dt + th G1 L_{M*} Δ_h + ta Adv(.; v^n)] phi^{n+1}
+        = phi^n/dt + L_{M*}( F'(phi*) - (1-th) G1 Δ_h phi^n )
+          - (1-ta) Adv(phi^n; v^n) + g_n(phi*, c^n)
+    with th = theta_ch, ta = theta_adv (1/2: Crank-Nicolson).  Returns (A, b, phi*)."""
     ny, nx = st.phi.shape
+    th, ta = ch_thetas(st, prm)
     phs = ex.phi_star(st.phi, st.phi_prev)
     Mx, My = ex.mobility_faces(phs, prm.Lambda)
     L_M = asm.flux_div(nx, ny, Mx, My)
     Lap = asm.lap(nx, ny, "mirror")
-    A = asm.ch_matrix(nx, ny, prm.dt, prm.Gamma1, Mx, My)
-    mu_e = ex.fprime(phs, prm.Gamma2).ravel() - 0.5 * prm.Gamma1 * (Lap @ st.phi.ravel())
+    A = asm.ch_matrix(nx, ny, prm.dt, prm.Gamma1, Mx, My, th, ta, st.u, st.v)
+    mu_e = ex.fprime(phs, prm.Gamma2).ravel() - (1.0 - th) * prm.Gamma1 * (Lap @ st.phi.ravel())
     b = (st.phi.ravel() / prm.dt + L_M @ mu_e
-         - ex.advection(phs, st.u, st.v).ravel()
+         - (1.0 - ta) * ex.advection(st.phi, st.u, st.v).ravel()
          + ex.growth(phs, st.c, prm.eps, prm.mu, prm.Kc).ravel())
     return A, b, phs
 
@@ -73,12 +83,14 @@ def nutrient_system(st: State, phi1: np.ndarray, prm: Params):
     consumption, explicit advection of phi_s c at level n:
       [diag(phi_s^{n+1}/dt + A/2 phi_n^{1/2}) - 1/2 L_K] c^{n+1}
         = phi_s^n c^n/dt - div_h(phi_s^n c^n v^n) + 1/2 L_K c^n - A/2 phi_n^{1/2} c^n,
-    K = D_s phi_s^{1/2} on faces."""
+    K = D_s phi_s^{1/2} on faces; phi_n^{1/2} = clip((phi^n + phi^{n+1})/2),
+    phi_s = 1 - clip(phi) (volume fractions, R24)."""
     ny, nx = st.phi.shape
-    ph = 0.5 * (st.phi + phi1)
+    vf = ex.volume_fraction
+    ph = vf(0.5 * (st.phi + phi1))
     sh = 1.0 - ph
-    s1 = 1.0 - phi1
-    s0 = 1.0 - st.phi
+    s1 = 1.0 - vf(phi1)
+    s0 = 1.0 - vf(st.phi)
     Kx = prm.Ds * 0.5 * (np.roll(sh, 1, axis=1) + sh)
     Ky = np.zeros((ny + 1, nx))
     Ky[1:ny] = prm.Ds * 0.5 * (sh[:-1] + sh[1:])
@@ -92,29 +104,33 @@ def nutrient_system(st: State, phi1: np.ndarray, prm: Params):
 
 
 def momentum_systems(st: State, phs: np.ndarray, prm: Params):
-    """Intermediate velocity (Eq. 19 with R restored, R6-R7), each component
-    divided through by nu = 1/(rho Re_a) to give an SPD system:
-      [a - 1/2 Δ_h^0] u* = a u^n + 1/2 Δ_h u^n + lid + (-(v^n·∇)u^n + R_x/rho)/nu,
-    a = 1/(nu dt); coefficients at phi* (R7)."""
+    """Intermediate velocity (Eq. 18-19 with R restored, R6-R7), per component,
+    SPD, th = theta_visc (1: the viscous term at u^{n+1}, the BVP of Eq. 19 as
+    printed), eta = 1/Re_a and rho at phi* (R6, R24):
+      [rho/dt - th div(eta grad)] u* = rho u^n/dt + (1-th) div(eta grad u^n) + th lid
+                                       - rho (v^n·∇)u^n + R_x,
+      R = -Gamma1 div(grad phi* grad phi*) + div(eta (grad v^n)^T)   (Eq. 17)."""
     ny, nx = st.phi.shape
     hy = 1.0 / ny
+    th = prm.theta_visc
     Rx, Ry = ex.phase_stress(phs, prm.Gamma1)
-    fu = ex.face_phi_u(phs)
-    fv = ex.face_phi_v(phs)
-    rho_u = ex.density(fu, prm.rho_n, prm.rho_s)
-    rho_v = ex.density(fv, prm.rho_n, prm.rho_s)
-    nu_u = ex.inv_reynolds(fu, prm.Re_n, prm.Re_s) / rho_u
-    nu_v = ex.inv_reynolds(fv, prm.Re_n, prm.Re_s) / rho_v
-    a_u = 1.0 / (nu_u * prm.dt)
-    a_v = 1.0 / (nu_v * prm.dt)
+    Tx, Ty = ex.visc_transpose(st.u, st.v, phs, prm.Re_n, prm.Re_s)
+    rho_u = ex.density(ex.face_phi_u(phs), prm.rho_n, prm.rho_s)
+    rho_v = ex.density(ex.face_phi_v(phs), prm.rho_n, prm.rho_s)
+    eta_u = ex.viscosity_u(phs, prm.Re_n, prm.Re_s)
+    eta_v = ex.viscosity_v(phs, prm.Re_n, prm.Re_s)
+    a_u = rho_u / prm.dt
+    a_v = rho_v / prm.dt
     Cu = ex.convective_u(st.u, st.v, prm.lid_u)
     Cv = ex.convective_v(st.u, st.v)
-    bu = a_u * st.u + 0.5 * ex.lap_u_inhom(st.u, prm.lid_u) + (-Cu + Rx / rho_u) / nu_u
-    bu[-1] += prm.lid_u / hy ** 2          # implicit half of the lid ghost (R3)
-    bv = a_v * st.v + 0.5 * ex.lap_v(st.v) + (-Cv + Ry / rho_v) / nu_v
+    bu = (a_u * st.u + (1.0 - th) * ex.visc_u_inhom(st.u, eta_u, prm.lid_u)
+          - rho_u * Cu + Rx + Tx)
+    Ku = ex.node_fluxes(eta_u)
+    bu[-1] += th * Ku[3][-1] * 2.0 * prm.lid_u / hy ** 2   # implicit part of the lid ghost (R3)
+    bv = a_v * st.v + (1.0 - th) * ex.visc_v(st.v, eta_v) - rho_v * Cv + Ry + Ty
     bv[0] = 0.0
-    Au = asm.u_matrix(nx, ny, a_u)
-    Av = asm.v_matrix(nx, ny, a_v)
+    Au = asm.u_matrix(nx, ny, a_u, Ku, th)
+    Av = asm.v_matrix(nx, ny, a_v, ex.node_fluxes(eta_v), th)
     return (Au, bu.ravel()), (Av, bv.ravel())
 
 

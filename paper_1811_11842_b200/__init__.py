@@ -26,7 +26,9 @@ __all__ = ["Simulation", "SimParams", "CHError", "unique_id"]
 @dataclass
 class SimParams:
     """ch_params with PAPER.md §5 defaults (lines 271-274), DESIGN.md R8-R10, R13;
-    refine = CG restarts until the true residual meets rtol (R21, 0 = off)."""
+    theta_* = implicit weights (R5, R7, R12), startup_be = backward-Euler
+    start-up steps (R23); refine = CG restarts until the true residual meets
+    rtol (R21, 0 = off)."""
     dt: float = 1e-4
     Gamma1: float = 33.467
     Gamma2: float = 1.25e6
@@ -42,10 +44,14 @@ class SimParams:
     rho_s: float = 1.0
     lid_u: float = 1.0
     rtol: float = 1e-10
+    theta_ch: float = 0.5
+    theta_adv: float = 0.5
+    theta_visc: float = 1.0
     maxit: int = 200000
     ch_solver: str = "bicgstab"
     gmres_restart: int = 30
     refine: int = 0
+    startup_be: int = 2
 
     def to_c(self) -> _lib.Params:
         p = _lib.Params()
@@ -148,6 +154,16 @@ class Simulation:
                 buf = np.empty(self.shape)
             out[n] = self.get_field(n, buf)
         return out
+
+    @property
+    def time_index(self) -> int:
+        n = C.c_int64()
+        self._check(lib.ch_get_time_index(self._h, C.byref(n)))
+        return n.value
+
+    @time_index.setter
+    def time_index(self, n: int):
+        self._check(lib.ch_set_time_index(self._h, int(n)))
 
     def step(self, n: int = 1):
         self._check(lib.ch_step(self._h, n))

@@ -31,9 +31,9 @@ class Grid(C.Structure):
 class Params(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("dt", "Gamma1", "Gamma2", "Lambda", "mu", "Kc", "eps",
                                           "A", "Ds", "Re_s", "Re_n", "rho_n", "rho_s", "lid_u",
-                                          "rtol")] + \
+                                          "rtol", "theta_ch", "theta_adv", "theta_visc")] + \
                [("maxit", C.c_int32), ("ch_solver", C.c_int32), ("gmres_restart", C.c_int32),
-                ("refine", C.c_int32)]
+                ("refine", C.c_int32), ("startup_be", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -73,12 +73,15 @@ lib.ch_solve.argtypes = [_P, C.c_int, _P, _P, C.c_int]
 lib.ch_get_stats.argtypes = [_P, C.POINTER(Stats)]
 lib.ch_reset_stats.argtypes = [_P]
 lib.ch_enable_timing.argtypes = [_P, C.c_int]
+lib.ch_set_time_index.argtypes = [_P, C.c_int64]
+lib.ch_get_time_index.argtypes = [_P, C.POINTER(C.c_int64)]
 
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = ("ch_create", "ch_comm_unique_id", "ch_comm_init", "ch_local_rows", "ch_partition", "ch_set_stream",
            "ch_set_fields", "ch_set_field", "ch_step", "ch_get_fields", "ch_get_field",
            "ch_apply_operator", "ch_solve", "ch_get_stats", "ch_reset_stats", "ch_enable_timing",
-           "ch_last_error", "ch_abi_version", "ch_destroy")
+           "ch_last_error", "ch_abi_version", "ch_destroy", "ch_set_time_index",
+           "ch_get_time_index")
 
 
 class CHError(RuntimeError):

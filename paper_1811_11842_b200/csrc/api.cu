@@ -37,7 +37,7 @@ struct Slab {
   Geom g;
   double* a[A_N];
   std::vector<double*> V;  // GMRES basis (m + 1 vectors) + work
-  std::vector<void*> bases;  // cudaMalloc'd blocks behind a[] (arrays may start skewed)
+  std::vector<void*> bases;  // cudaMalloc'd blocks behind a[]
 };
 
 struct Timer {
@@ -78,20 +78,15 @@ struct ch_handle {
   double* cgtab = nullptr;    // deferred-p/x CG coefficient tables, device [NSC][2][CGT]
   unsigned int* pbar = nullptr; // persistent-CG grid barrier: count, generation, abort flag
   int persist = 0;            // single-slab CG solves as one cooperative launch (env CHB_PERSIST)
-  int px_async = 0;           // p/x updates on a side stream, overlapped with the sweeps
-                              // (block length m/2, z ring 2m/2+1; env CHB_PXASYNC)
   int cur_m = 0;              // block length of the solve in flight (0: cg_defer)
-  cudaStream_t st2 = nullptr; // side stream of the asynchronous p/x updates
-  cudaEvent_t pxev[5] = {};   // [0..3] p/x done per block (mod 4), [4] sweep-side marker
   int cg_defer = 64;          // block length m (2..64) of the deferred p/x CG (env CHB_DEFER);
                               // reduced at ch_create if the z history would not fit
   double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
   double* gm_host = nullptr;  // pinned mirror
   int cg3 = 1;                // single-reduction CG: three-term z recurrence (env CHB_CG3)
-  int vec = 3;                // CG: 3 single-reduction fused TMA sweep; two-kernel HS-CG with
-                              // 2 TMA ring, 1 register pipeline, 0 scalar (env CHB_VEC)
   int strip2 = 0;             // rows per strip, 0 = one resident wave (env CHB_STRIP)
   int pdl = 1;                // programmatic dependent launch of the CG sweeps (env CHB_PDL)
+  int64_t tidx = 0;           // time index n of the state (ch_set_time_index; R23 start-up)
 };
 
 namespace {
@@ -112,12 +107,25 @@ namespace {
     if (s_ != CH_OK) return s_; \
   } while (0)
 
+// Parameters of the step at time index n: the CH and advection weights are 1
+// during the backward-Euler start-up steps (R23).
+Phys phys_at(const ch_params& p, int64_t n);
+
 Phys phys(const ch_params& p) {
   Phys ph;
   ph.dt = p.dt; ph.Gamma1 = p.Gamma1; ph.Gamma2 = p.Gamma2; ph.Lambda = p.Lambda;
   ph.mu = p.mu; ph.Kc = p.Kc; ph.eps = p.eps; ph.A = p.A; ph.Ds = p.Ds;
   ph.Re_s = p.Re_s; ph.Re_n = p.Re_n; ph.rho_n = p.rho_n; ph.rho_s = p.rho_s;
   ph.lid_u = p.lid_u;
+  ph.th_ch = p.theta_ch;
+  ph.th_adv = p.theta_adv;
+  ph.th_visc = p.theta_visc;
+  return ph;
+}
+
+Phys phys_at(const ch_params& p, int64_t n) {
+  Phys ph = phys(p);
+  if (n < p.startup_be) ph.th_ch = ph.th_adv = 1.0;
   return ph;
 }
 
@@ -329,8 +337,22 @@ int solve_status(ch_handle* h, int sys, const char* name) {
   h->stats.iters_last[sys] = s.iter;
   h->stats.iters_total[sys] += s.iter;
   h->stats.resid_last[sys] = s.bb > 0 ? sqrt(s.rr / s.bb) : 0.0;
-  if (s.status == 1) {
-    h->err = std::string(name) + ": Krylov breakdown";
+  if (s.status == 1 || s.status >= 3) {
+    static const char* what[] = {
+        "", "zero or non-finite inner product", "",
+        "(r, z) <= 0 or non-finite (operator or preconditioner not SPD?)",
+        "(A z, z) <= 0 or non-finite (operator not SPD?)",
+        "CG step denominator delta - beta gamma/alpha <= 0",
+        "three-term recurrence omega non-finite",
+        "BiCGStab (r^, r) = 0 or non-finite",
+        "BiCGStab (r^, v) = 0 or non-finite",
+        "BiCGStab (t, t) = 0 or non-finite / omega = 0",
+        "residual norm non-finite (NaN/Inf in the iterates)"};
+    char buf[320];
+    snprintf(buf, sizeof buf, "%s: Krylov breakdown at iteration %d of step %lld: %s "
+             "[value %.6e, |r|^2 %.6e, |b|^2 %.6e]", name, s.iter, (long long)h->tidx,
+             s.status <= 10 ? what[s.status] : "?", s.last, s.rr, s.bb);
+    h->err = buf;
     return CH_ERR_BREAKDOWN;
   }
   if (s.status == 2) {
@@ -356,7 +378,6 @@ OpDesc opdesc(ch_handle* h, int kind, const Slab& s) {
   d.kind = kind;
   d.strip = 16;
   d.strip2 = h->strip2;
-  d.vec = h->vec;
   d.pdl = h->pdl;
   d.a = nullptr;
   d.w = nullptr;
@@ -369,74 +390,9 @@ OpDesc opdesc(ch_handle* h, int kind, const Slab& s) {
     case OPK_POISSON_VAR: d.w = s.a[A_PHI1]; break;
     case OPK_NUTRIENT: d.a = s.a[A_CA]; d.w = s.a[A_CW]; d.s = 0.5; d.kscale = h->prm.Ds; break;
     case OPK_MOM_U:
-    case OPK_MOM_V: d.a = s.a[A_CA]; d.s = 0.5; break;
+    case OPK_MOM_V: d.a = s.a[A_CA]; d.w = s.a[A_CW]; d.s = h->prm.theta_visc; break;
   }
   return d;
-}
-
-int cg_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, int use_shift,
-             const char* name, int wid = -1) {
-  TRY(set_maxit(h, sys));
-  if (wid >= 0) TRY(halo(h, wid, 1));
-  TRY(halo(h, xid, 1));
-  {
-    KTime kt(h, CH_KC_CG_INIT, 40.0 * h->grid.nx * (double)h->nrows / h->S);
-    for (int s = 0; s < h->S; ++s) {
-      Slab& sl = h->sl[s];
-      launch_cg5_init(opdesc(h, kind, sl), sl.g, sl.a[xid], sl.a[bid], use_shift, sl.a[A_Z],
-                      rargs(h, FIN_CG_INIT, sys, s), h->st);
-    }
-  }
-  TRY(check_launch(h, "cg5_init"));
-  TRY(fin_slabs(h, FIN_CG_INIT, sys, 3));
-  TRY(halo(h, A_Z, 1));
-  const double cells = (double)h->grid.nx * (double)h->nrows / h->S;
-  long k = 1;
-  int chunk = 4;
-  for (;;) {
-    for (int it = 0; it < chunk; ++it, ++k) {
-      const int pold = (k & 1) ? A_PB : A_PA;
-      const int pnew = (k & 1) ? A_PA : A_PB;
-      {
-        KTime kt(h, CH_KC_CG_A, cg5_bytes_A(kind) * cells, k);
-        for (int s = 0; s < h->S; ++s) {
-          Slab& sl = h->sl[s];
-          launch_cg5_A(opdesc(h, kind, sl), sl.g, sl.a[A_Z], sl.a[pold], sl.a[pnew], sl.a[xid],
-                       k == 1, rargs(h, FIN_CG_A, sys, s), h->st);
-        }
-      }
-      TRY(fin_slabs(h, FIN_CG_A, sys, 1));
-      TRY(halo(h, pnew, 1));
-      {
-        KTime kt(h, CH_KC_CG_B, cg5_bytes_B(kind) * cells, k);
-        for (int s = 0; s < h->S; ++s) {
-          Slab& sl = h->sl[s];
-          launch_cg5_B(opdesc(h, kind, sl), sl.g, sl.a[pnew], sl.a[A_Z],
-                       rargs(h, FIN_CG_B, sys, s), h->st);
-        }
-      }
-      TRY(fin_slabs(h, FIN_CG_B, sys, 2));
-      TRY(halo(h, A_Z, 1));
-    }
-    TRY(check_launch(h, "cg5 iteration"));
-    TRY(poll(h, sys));
-    if (h->sch[sys].done) break;
-    if (chunk < 64) chunk *= 2;
-  }
-  const long K = h->sch[sys].iter;
-  const int plast = (K & 1) ? A_PA : A_PB;
-  {
-    KTime kt(h, CH_KC_VEC, 24.0 * cells);
-    for (int s = 0; s < h->S; ++s) {
-      Slab& sl = h->sl[s];
-      launch_cg5_finish(sl.g, sl.a[xid], sl.a[plast], nullspace, 0, rargs(h, FIN_MEAN, sys, s),
-                        h->st);
-    }
-  }
-  TRY(check_launch(h, "cg5_finish"));
-  if (nullspace) TRY(fin_slabs(h, FIN_MEAN, sys, 1));
-  harvest(h, K);
-  return solve_status(h, sys, name);
 }
 
 // ------------------------------------------- single-reduction CG (default)
@@ -450,16 +406,10 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   if (wid >= 0) TRY(halo(h, wid, 2));
   if (AM) TRY(halo(h, A_CA, 1));
   TRY(halo(h, xid, 1));
-  // z ring of m + 1 buffers (p/x deferred over blocks of m sweeps); with the
-  // asynchronous p/x the same buffers hold 2 m' + 1 z's of blocks m' = m / 2
-  const bool apx = h->px_async && !h->persist && h->cg_defer >= 4;
-  const int m = apx ? h->cg_defer / 2 : h->cg_defer;
-  const int NZ = apx ? 2 * m + 1 : m + 1;
+  // z ring of m + 1 buffers (p/x deferred over blocks of m sweeps)
+  const int m = h->cg_defer;
+  const int NZ = m + 1;
   h->cur_m = m;
-  if (apx && !h->st2) {
-    CK(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
-    for (auto& e : h->pxev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
   int Zr[CGM + 1];
   Zr[0] = A_Z;
   Zr[1] = A_R;
@@ -470,25 +420,6 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   auto px = [&](long k_last, int n, int write_p) -> int {
     // z_k of iterations k_last - n + 1 .. k_last
     const long k0 = k_last - n + 1;
-    if (apx && write_p) {
-      // side stream: starts when the block's last sweep is done; the main stream
-      // waits for it only m' - 1 sweeps later (before the finalize that reuses
-      // its coefficient table, and before its z's are overwritten)
-      const long b = k_last / m;
-      CK(cudaEventRecord(h->pxev[4], h->st));
-      CK(cudaStreamWaitEvent(h->st2, h->pxev[4], 0));
-      for (int s = 0; s < h->S; ++s) {
-        Slab& sl = h->sl[s];
-        ZList zl;
-        for (int j = 0; j < CGM; ++j) zl.z[j] = j < n ? sl.a[Zr[(k0 + j) % NZ]] : nullptr;
-        launch_cgs_px(sl.g, zl, n, k0 == 0, write_p, (int)(k_last + 1),
-                      tab + ((k_last / m) & 1) * CGT, h->sc + sys, sl.a[P], sl.a[xid], h->st2);
-      }
-      h->stats.launches += h->S;
-      h->stats.kc_launches[CH_KC_CG_PX] += h->S;
-      CK(cudaEventRecord(h->pxev[b & 3], h->st2));
-      return check_launch(h, "cgs_px async");
-    }
     KTime kt(h, CH_KC_CG_PX, 8.0 * (n + 4) * cells);
     for (int s = 0; s < h->S; ++s) {
       Slab& sl = h->sl[s];
@@ -570,8 +501,6 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   for (;;) {
     for (int it = 0; it < chunk; ++it, ++k) {
       const int first = (k == 0), dir = (k & 1) ? -1 : 1;
-      if (apx && (k + 1) % m == 0 && k + 1 >= 2 * m)  // block (k+1)/m - 2's p/x must be done
-        CK(cudaStreamWaitEvent(h->st, h->pxev[((k + 1) / m - 2) & 3], 0));
       const int zi = Zr[k % NZ], zo = Zr[(k + 1) % NZ];
       // three-term: the sweep reads z_{k-1} (still in the ring) instead of s_{k-1}
       // and writes no s
@@ -595,10 +524,6 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   }
   }
   const long K = h->sch[sys].iter;
-  if (apx) {  // every asynchronous p/x launched so far is done before the tail
-    CK(cudaEventRecord(h->pxev[4], h->st2));
-    CK(cudaStreamWaitEvent(h->st, h->pxev[4], 0));
-  }
   if (K > 0 && K % m != 0) TRY(px(K - 1, (int)(K % m), 0));
   {
     KTime kt(h, CH_KC_VEC, 24.0 * cells);
@@ -616,9 +541,7 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
 
 int cg_once(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, int use_shift,
             const char* name, int wid) {
-  if (h->vec == 3 && (h->grid.nx % 2 == 0))
-    return cgs_solve(h, sys, kind, xid, bid, nullspace, use_shift, name, wid);
-  return cg_solve(h, sys, kind, xid, bid, nullspace, use_shift, name, wid);
+  return cgs_solve(h, sys, kind, xid, bid, nullspace, use_shift, name, wid);
 }
 
 // CG with optional true-residual refinement (params.refine): each restart's
@@ -652,12 +575,17 @@ int cg_any(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, int
 
 // ------------------------------------------------------------ BiCGStab (CH)
 ChCoef chcoef(ch_handle* h, const Slab& s, bool precond) {
+  const Phys ph = phys_at(h->prm, h->tidx);
   ChCoef c;
   c.phis = s.a[A_PHIS];
   c.dinv = precond ? s.a[A_DINV] : nullptr;
+  c.u = ph.th_adv != 0.0 ? s.a[A_U] : nullptr;
+  c.v = s.a[A_V];
   c.dt = h->prm.dt;
-  c.g1h = 0.5 * h->prm.Gamma1;
+  c.g1t = ph.th_ch * h->prm.Gamma1;
   c.Lambda = h->prm.Lambda;
+  c.tha = ph.th_adv;
+  c.strip = h->strip2;
   return c;
 }
 
@@ -753,7 +681,7 @@ int bicgstab_or_gmres(ch_handle* h, int xid, int bid) {
 
 // ------------------------------------------------------------- one step
 int step_once(ch_handle* h) {
-  const Phys ph = phys(h->prm);
+  const Phys ph = phys_at(h->prm, h->tidx);
   const double cells = (double)h->grid.nx * (double)h->nrows / h->S;
   // 1. Cahn-Hilliard
   TRY(halo(h, A_PHI, 2));
@@ -783,18 +711,20 @@ int step_once(ch_handle* h) {
   // 3. intermediate velocity
   {
     KTime kt(h, CH_KC_RHS, 40.0 * cells);
-    for (auto& s : h->sl) launch_mom_rhs_u(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_B], h->st);
+    for (auto& s : h->sl)
+      launch_mom_rhs_u(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_CW], s.a[A_B], h->st);
   }
   TRY(check_launch(h, "mom_rhs_u"));
   TRY(copy_arr(h, A_U, A_US));
-  TRY(cg_any(h, CH_SYS_U, OPK_MOM_U, A_US, A_B, 0, 0, "momentum-u"));
+  TRY(cg_any(h, CH_SYS_U, OPK_MOM_U, A_US, A_B, 0, 0, "momentum-u", A_CW));
   {
     KTime kt(h, CH_KC_RHS, 40.0 * cells);
-    for (auto& s : h->sl) launch_mom_rhs_v(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_B], h->st);
+    for (auto& s : h->sl)
+      launch_mom_rhs_v(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_CW], s.a[A_B], h->st);
   }
   TRY(check_launch(h, "mom_rhs_v"));
   TRY(copy_arr(h, A_V, A_VS));
-  TRY(cg_any(h, CH_SYS_V, OPK_MOM_V, A_VS, A_B, 0, 0, "momentum-v"));
+  TRY(cg_any(h, CH_SYS_V, OPK_MOM_V, A_VS, A_B, 0, 0, "momentum-v", A_CW));
   // 4. pressure Poisson with the constant null space
   TRY(halo(h, A_US, 1));
   TRY(halo(h, A_VS, 1));
@@ -829,6 +759,7 @@ int step_once(ch_handle* h) {
   }
   harvest(h, -1);
   h->stats.steps += 1;
+  h->tidx += 1;
   return CH_OK;
 }
 
@@ -1090,9 +1021,6 @@ static void destroy_mem(ch_handle* h) {
   if (h->gm_dev) cudaFree(h->gm_dev);
   if (h->cgtab) cudaFree(h->cgtab);
   if (h->pbar) cudaFree(h->pbar);
-  for (auto& e : h->pxev)
-    if (e) cudaEventDestroy(e);
-  if (h->st2) cudaStreamDestroy(h->st2);
   if (h->gm_host) cudaFreeHost(h->gm_host);
   for (auto& r : h->tm.pending) {
     cudaEventDestroy(r.e0);
@@ -1117,26 +1045,29 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   };
   if (!grid || !params) return fail(CH_ERR_ARG, nullptr, "null argument");
   const ch_grid G = *grid;
-  if (G.nx < 4 || G.ny < 4 || G.nranks < 1 || G.rank < 0 || G.rank >= G.nranks)
-    return fail(CH_ERR_ARG, nullptr, "bad grid (need nx, ny >= 4, 0 <= rank < nranks)");
+  if (G.nx < 4 || G.ny < 4 || (G.nx & 1) || G.nranks < 1 || G.rank < 0 || G.rank >= G.nranks)
+    return fail(CH_ERR_ARG, nullptr, "bad grid (need even nx >= 4, ny >= 4, 0 <= rank < nranks)");
   const int S = G.virtual_slabs < 1 ? 1 : G.virtual_slabs;
   const int total = G.nranks * S;
   if (G.ny < 2 * total) return fail(CH_ERR_ARG, nullptr, "too many slabs for ny (>= 2 rows each)");
   if (!(params->dt > 0) || !(params->rtol > 0) || params->maxit < 1)
     return fail(CH_ERR_ARG, nullptr, "bad params (dt > 0, rtol > 0, maxit >= 1)");
+  if (!(params->theta_ch >= 0 && params->theta_ch <= 1) ||
+      !(params->theta_adv >= 0 && params->theta_adv <= 1) ||
+      !(params->theta_visc > 0 && params->theta_visc <= 1) || params->startup_be < 0)
+    return fail(CH_ERR_ARG, nullptr,
+                "bad params (theta_ch, theta_adv in [0,1], theta_visc in (0,1], startup_be >= 0)");
   if (cudaSetDevice(G.device) != cudaSuccess) return fail(CH_ERR_CUDA, nullptr, "cudaSetDevice");
   ch_handle* h = new ch_handle();
   h->grid = G;
   h->prm = *params;
   h->S = S;
   h->nslabs_total = total;
-  if (const char* e = getenv("CHB_VEC")) h->vec = atoi(e);
   if (const char* e = getenv("CHB_CG3")) h->cg3 = atoi(e) != 0;
   if (const char* e = getenv("CHB_STRIP")) h->strip2 = std::max(0, atoi(e));
   if (const char* e = getenv("CHB_PDL")) h->pdl = atoi(e) != 0;
   if (const char* e = getenv("CHB_DEFER")) h->cg_defer = std::min(std::max(2, atoi(e)), CGM);
   if (const char* e = getenv("CHB_PERSIST")) h->persist = atoi(e) != 0;
-  if (const char* e = getenv("CHB_PXASYNC")) h->px_async = atoi(e) != 0;
   memset(&h->stats, 0, sizeof(ch_stats));
   // rows: balanced split of ny over `total` slabs (first ny % total get one more)
   const int base = G.ny / total, rem = G.ny % total;
@@ -1178,22 +1109,14 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
     sl.g.ihx2 = (double)G.nx * G.nx;
     sl.g.ihy2 = (double)G.ny * G.ny;
     for (int i = 0; i < A_N; ++i) sl.a[i] = nullptr;
-    // z history: only the m - 1 buffers the chosen block length needs.
-    // Array i starts i * skew bytes (mod 64 KiB) into its block, so that the
-    // same cell of different arrays does not map to the same DRAM channel
-    // phase (env CHB_SKEW, bytes, multiple of 256)
+    // z history: only the m - 1 buffers the chosen block length needs
     const int n_alloc = A_ZH0 + std::max(0, h->cg_defer - 1);
-    long skew = 0;
-    if (const char* e = getenv("CHB_SKEW")) skew = (atol(e) / 256) * 256;
-    if (skew < 0) skew = 0;
-    const size_t pad = skew ? 65536 : 0;
     for (int i = 0; i < n_alloc; ++i) {
       void* base = nullptr;
-      if (cudaMalloc(&base, h->arr_elems * sizeof(double) + pad) != cudaSuccess)
+      if (cudaMalloc(&base, h->arr_elems * sizeof(double)) != cudaSuccess)
         return fail(CH_ERR_CUDA, h, "cudaMalloc (out of device memory?)");
       sl.bases.push_back(base);
-      const size_t off_b = skew ? ((size_t)i * (size_t)skew) % 65536 : 0;
-      sl.a[i] = reinterpret_cast<double*>(static_cast<char*>(base) + off_b);
+      sl.a[i] = static_cast<double*>(base);
       cudaMemset(sl.a[i], 0, h->arr_elems * sizeof(double));
     }
   }
@@ -1296,6 +1219,18 @@ int ch_get_fields(ch_handle* h, double* phi, double* c, double* u, double* v, do
   return CH_OK;
 }
 
+int ch_set_time_index(ch_handle* h, int64_t n) {
+  if (!h || n < 0) return CH_ERR_ARG;
+  h->tidx = n;
+  return CH_OK;
+}
+
+int ch_get_time_index(const ch_handle* h, int64_t* n) {
+  if (!h || !n) return CH_ERR_ARG;
+  *n = h->tidx;
+  return CH_OK;
+}
+
 int ch_step(ch_handle* h, int nsteps) {
   if (!h || nsteps < 0) return CH_ERR_ARG;
   for (int n = 0; n < nsteps; ++n) TRY(step_once(h));
@@ -1306,7 +1241,7 @@ namespace {
 // Coefficients of operator `op` from the current state (what ch_step would
 // use for its first solve of that kind); returns the 5-point kind or -1 (CH).
 int prep_operator(ch_handle* h, int op, int* kind) {
-  const Phys ph = phys(h->prm);
+  const Phys ph = phys_at(h->prm, h->tidx);
   TRY(halo(h, A_PHI, 2));
   TRY(halo(h, A_PHIP, 2));
   TRY(halo(h, A_U, 1));
@@ -1327,9 +1262,9 @@ int prep_operator(ch_handle* h, int op, int* kind) {
     case CH_OP_MOM_V:
       for (auto& s : h->sl) {
         if (op == CH_OP_MOM_U)
-          launch_mom_rhs_u(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_TMP2], h->st);
+          launch_mom_rhs_u(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_CW], s.a[A_TMP2], h->st);
         else
-          launch_mom_rhs_v(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_TMP2], h->st);
+          launch_mom_rhs_v(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_CW], s.a[A_TMP2], h->st);
       }
       *kind = (op == CH_OP_MOM_U) ? OPK_MOM_U : OPK_MOM_V;
       break;
@@ -1357,7 +1292,9 @@ int ch_apply_operator(ch_handle* h, int op, const double* x, double* y, int wher
     }
   } else {
     TRY(halo(h, A_TMP, 1));
-    const double bpc = kind == OPK_POISSON_CONST ? 16.0 : 24.0;   // x, y (+ coefficient)
+    if (kind == OPK_MOM_U || kind == OPK_MOM_V) TRY(halo(h, A_CW, 1));
+    // x, y (+ w) (+ a)
+    const double bpc = kind == OPK_POISSON_CONST ? 16.0 : (kind == OPK_POISSON_VAR ? 24.0 : 32.0);
     KTime kt(h, CH_KC_OP_APPLY, bpc * cells);
     for (auto& s : h->sl) launch_op5_apply(opdesc(h, kind, s), s.g, s.a[A_TMP], s.a[A_B], h->st);
   }
@@ -1389,7 +1326,7 @@ int ch_solve(ch_handle* h, int op, const double* b, double* x, int where) {
       TRY(fin_slabs(h, FIN_MEAN, sys, 1));
     }
     TRY(cg_any(h, sys, kind, A_US, A_B, ns, ns, "solve",
-               kind == OPK_POISSON_VAR ? A_PHI1 : -1));
+               kind == OPK_POISSON_VAR ? A_PHI1 : (ns ? -1 : A_CW)));
     if (ns)
       for (auto& s : h->sl) launch_sub_mean(s.g, s.a[A_US], h->sc + sys, h->st);
   }

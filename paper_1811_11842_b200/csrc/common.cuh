@@ -177,6 +177,28 @@ struct CoefReq {
 };
 
 __device__ __forceinline__ bool bad(double x) { return !(x == x) || x == 0.0; }
+// CG on an SPD operator: (r, z), (A z, z) and the step denominator are > 0
+// and finite; anything else means an indefinite operator or lost arithmetic.
+__device__ __forceinline__ bool not_pos(double x) { return !(x > 0.0) || !(x < 1e308); }
+
+// Breakdown codes in KScal.status (>= 3; 1 = generic, 2 = maxit), the value
+// that tripped is left in KScal.last (reported by ch_last_error).
+enum KStatus : int {
+  KS_OK = 0, KS_BREAK = 1, KS_MAXIT = 2,
+  KS_CG_GAMMA = 3,   // (r, z) <= 0 or not finite
+  KS_CG_DELTA = 4,   // (A z, z) <= 0 or not finite
+  KS_CG_DEN = 5,     // alpha's denominator delta - beta gamma / alpha <= 0
+  KS_CG_OMEGA = 6,   // three-term recurrence omega not finite
+  KS_BI_RHO = 7,     // BiCGStab (r^, r) = 0 or not finite
+  KS_BI_RV = 8,      // BiCGStab (r^, v) = 0 or not finite
+  KS_BI_TT = 9,      // BiCGStab (t, t) = 0 or not finite, or omega = 0
+  KS_RES_NAN = 10    // residual norm not finite
+};
+__device__ __forceinline__ void kfail(KScal* s, int code, double val) {
+  s->status = code;
+  s->last = val;
+  s->done = 1;
+}
 
 __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx& fc,
                                 CoefReq* req = nullptr) {
@@ -223,7 +245,7 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
       break;
     }
     case FIN_BI_ALPHA: {
-      if (bad(t[0])) { s->status = 1; s->done = 1; break; }
+      if (bad(t[0])) { kfail(s, KS_BI_RV, t[0]); break; }
       s->alpha = s->rho / t[0];
       break;
     }
@@ -234,7 +256,7 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
     }
     case FIN_BI_OMEGA: {
       if (s->half) break;
-      if (bad(t[1])) { s->status = 1; s->done = 1; break; }
+      if (bad(t[1])) { kfail(s, KS_BI_TT, t[1]); break; }
       s->omega = t[0] / t[1];
       break;
     }
@@ -243,8 +265,10 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
       if (s->half) { s->done = 1; break; }
       s->rr = t[0];
       if (t[0] <= s->tol2) { s->done = 1; break; }
+      if (!(t[0] < 1e308)) { kfail(s, KS_RES_NAN, t[0]); break; }
       if (s->iter >= s->maxit) { s->status = 2; s->done = 1; break; }
-      if (t[1] == 0.0 || !(t[1] == t[1]) || s->omega == 0.0) { s->status = 1; s->done = 1; break; }
+      if (s->omega == 0.0) { kfail(s, KS_BI_TT, s->omega); break; }
+      if (bad(t[1])) { kfail(s, KS_BI_RHO, t[1]); break; }
       s->rho_prev = s->rho;
       s->rho = t[1];
       break;
@@ -255,7 +279,7 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
     }
     case FIN_CGS_D0: {
       if (s->done) break;
-      if (bad(t[0])) { s->status = 1; s->done = 1; break; }
+      if (not_pos(t[0])) { kfail(s, KS_CG_DELTA, t[0]); break; }
       s->alpha = s->rho / t[0];
       s->beta = 0.0;
       s->aux[0] = 0.0;
@@ -270,16 +294,18 @@ __device__ inline void finalize(int fin, const double* t, KScal* s, const FinCtx
       s->iter += 1;
       s->rr = t[1];
       if (t[1] <= s->tol2) { s->done = 1; break; }
+      if (!(t[1] < 1e308)) { kfail(s, KS_RES_NAN, t[1]); break; }
       if (s->iter >= s->maxit) { s->status = 2; s->done = 1; break; }
-      if (bad(t[0]) || bad(s->rho) || bad(s->alpha)) { s->status = 1; s->done = 1; break; }
+      if (not_pos(t[0])) { kfail(s, KS_CG_GAMMA, t[0]); break; }
+      if (not_pos(t[2])) { kfail(s, KS_CG_DELTA, t[2]); break; }
       const double beta = t[0] / s->rho;
       const double den = t[2] - beta * t[0] / s->alpha;
-      if (bad(den)) { s->status = 1; s->done = 1; break; }
+      if (not_pos(den)) { kfail(s, KS_CG_DEN, den); break; }
       // three-term z recurrence (Concus-Golub-O'Leary form, kernels_cgs.cu):
       // gamma' = mu'/nu', omega' = 1 / (1 - (gamma'/gamma) (mu'/mu) / omega)
       const double gnew = t[0] / t[2];
       const double om = 1.0 / (1.0 - (gnew / s->aux[4]) * (t[0] / s->rho) / s->aux[5]);
-      if (bad(gnew) || !(fabs(om) < 1e300)) { s->status = 1; s->done = 1; break; }
+      if (!(fabs(om) < 1e300)) { kfail(s, KS_CG_OMEGA, om); break; }
       s->aux[4] = gnew;
       s->aux[5] = om;
       s->aux[0] = s->alpha;  // alpha_{i} for the in-sweep x update over pairs
@@ -363,23 +389,27 @@ __device__ inline void finalize_cgs_pre(const double* t, const CgsPre& p, const 
                                         KScal* s, const FinCtx& fc, int lane) {
   const int iter = p.iter + 1;
   int done = 0, status = 0;
-  double beta = 0.0, alpha = 0.0, gnew = 0.0, om = 0.0;
+  double beta = 0.0, alpha = 0.0, gnew = 0.0, om = 0.0, val = 0.0;
   if (t[1] <= p.tol2) {
     done = 1;
+  } else if (!(t[1] < 1e308)) {
+    status = KS_RES_NAN, val = t[1], done = 1;
   } else if (iter >= p.maxit) {
-    status = 2;
+    status = KS_MAXIT;
     done = 1;
-  } else if (bad(t[0]) || bad(p.rho) || bad(p.alpha)) {
-    status = 1;
-    done = 1;
+  } else if (not_pos(t[0])) {
+    status = KS_CG_GAMMA, val = t[0], done = 1;
+  } else if (not_pos(t[2])) {
+    status = KS_CG_DELTA, val = t[2], done = 1;
   } else {
     beta = t[0] / p.rho;
     const double den = t[2] - beta * t[0] / p.alpha;
     gnew = t[0] / t[2];
     om = 1.0 / (1.0 - (gnew / p.aux4) * (t[0] / p.rho) / p.aux5);
-    if (bad(den) || bad(gnew) || !(fabs(om) < 1e300)) {
-      status = 1;
-      done = 1;
+    if (not_pos(den)) {
+      status = KS_CG_DEN, val = den, done = 1;
+    } else if (!(fabs(om) < 1e300)) {
+      status = KS_CG_OMEGA, val = om, done = 1;
     } else {
       alpha = t[0] / den;
     }
@@ -388,7 +418,10 @@ __device__ inline void finalize_cgs_pre(const double* t, const CgsPre& p, const 
     s->iter = iter;
     s->rr = t[1];
     if (done) {
-      if (status) s->status = status;
+      if (status) {
+        s->status = status;
+        s->last = val;
+      }
       s->done = 1;
     } else {
       s->aux[4] = gnew;

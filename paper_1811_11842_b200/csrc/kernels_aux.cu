@@ -1,0 +1,263 @@
+// kernels_aux.cu -- once-per-solve kernels of the 5-point symmetric operator
+// family (pressure Poisson, Eq. 20; intermediate velocity, Eq. 19; nutrient,
+// Eq. 16) around the fused single-reduction CG sweep of kernels_cgs.cu:
+//
+//   y = a x + s * sum_faces k_f (x - x_nb) / h_f^2         (op5.cuh)
+//
+// Operator instances (OpKind):
+//   POISSON_CONST  a = 0, s = 1, k = 1                      (rho_n == rho_s)
+//   POISSON_VAR    a = 0, s = 1, k = 1/rho(face mean phi^{n+1})
+//   NUTRIENT       a = a_c[], s = 1/2, k = D_s * face mean(phi_s^{1/2})
+//   MOM_U          a = rho/dt[], s = theta_visc, k = face mean(eta), odd-reflection walls
+//   MOM_V          a = rho/dt[], s = theta_visc, k = face mean(eta), Dirichlet wall faces,
+//                  row 0 = identity          (eta = 1/Re_a at the unknown's points, R6)
+//
+// CG initialisation (r = b - A x, z = D^-1 r, three reductions), the plain
+// operator apply of ch_apply_operator, the CG finish / null-space mean, and
+// the cross-slab finalize.  Each thread owns one column and marches down a
+// strip of rows keeping the three-row window in registers; x-neighbours come
+// from warp shuffles (edge lanes and the periodic seam reload through L1).
+#include "common.cuh"
+#include "launch.h"
+#include "op5.cuh"
+
+namespace chb {
+
+// ---------------------------------------------------------------------------
+// Column-marching helpers.  All threads of a block run the same row loop.
+struct Col {
+  int c, cc, cw, ce, lane;
+  bool act, needW, needE;
+  __device__ __forceinline__ Col(const Geom& g) {
+    lane = threadIdx.x & 31;
+    c = blockIdx.x * blockDim.x + threadIdx.x;
+    act = c < g.nx;
+    cc = act ? c : g.nx - 1;
+    cw = wrapc(cc - 1, g.nx);
+    ce = wrapc(cc + 1, g.nx);
+    needW = (lane == 0) || (c == 0);
+    needE = (lane == 31) || (c + 1 >= g.nx);
+  }
+};
+
+#define CHB_SHFL_W(v) __shfl_up_sync(FULL, (v), 1)
+#define CHB_SHFL_E(v) __shfl_down_sync(FULL, (v), 1)
+
+// ------------------------------------------------------------------ CG init
+// r = (b - shift) - A x;  z = r / d;  reduce ||b - shift||^2, (r, z), (r, r)
+template <int BC, int AM, int KM>
+__global__ void __launch_bounds__(128) k_cg5_init(Geom g, Op5T op, const double* __restrict__ x,
+                                                  const double* __restrict__ b, int use_shift,
+                                                  double* __restrict__ z, int strip, RedArgs ra) {
+  const double shift = use_shift ? ra.sc->mean : 0.0;
+  Col col(g);
+  const int jl0 = blockIdx.y * strip, jl1 = min(jl0 + strip, g.nyl);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  int gj = g.j0 + jl0;
+  double xm = ldf<BC>(x, g, gj - 1, col.cc), x0 = ldf<BC>(x, g, gj, col.cc);
+  double wm = 0.0, w0 = 0.0;
+  if (KM) {
+    wm = ldf<BC_MIRROR>(op.w, g, gj - 1, col.cc);
+    w0 = ldf<BC_MIRROR>(op.w, g, gj, col.cc);
+  }
+  for (int jl = jl0; jl < jl1; ++jl, ++gj) {
+    const double xp = ldf<BC>(x, g, gj + 1, col.cc);
+    double xw = CHB_SHFL_W(x0), xe = CHB_SHFL_E(x0);
+    if (col.needW) xw = ldf<BC>(x, g, gj, col.cw);
+    if (col.needE) xe = ldf<BC>(x, g, gj, col.ce);
+    double wp = 0.0, ww = 0.0, we = 0.0;
+    if (KM) {
+      wp = ldf<BC_MIRROR>(op.w, g, gj + 1, col.cc);
+      ww = CHB_SHFL_W(w0);
+      we = CHB_SHFL_E(w0);
+      if (col.needW) ww = ldf<BC_MIRROR>(op.w, g, gj, col.cw);
+      if (col.needE) we = ldf<BC_MIRROR>(op.w, g, gj, col.ce);
+    }
+    const double ac = AM ? op.a[off(g, gj, col.cc)] : 0.0;
+    double y, d;
+    eval5T<BC, AM, KM>(op, g, gj, ac, w0, ww, we, wm, wp, x0, xw, xe, xm, xp, y, d);
+    if (col.act) {
+      const size_t o = off(g, gj, col.c);
+      const double bc = b[o] - ((BC == BC_VFACE && gj == 0) ? 0.0 : shift);
+      const double r = bc - y;
+      const double zz = r / d;
+      z[o] = zz;
+      s0 += bc * bc;
+      s1 += r * zz;
+      s2 += r * r;
+    }
+    xm = x0;
+    x0 = xp;
+    wm = w0;
+    w0 = wp;
+  }
+  double v[3] = {s0, s1, s2};
+  block_reduce_finalize<3>(v, ra);
+}
+
+// --------------------------------------------------------------- plain apply
+template <int BC, int AM, int KM>
+__global__ void __launch_bounds__(128) k_op5_apply(Geom g, Op5T op, const double* __restrict__ x,
+                                                   double* __restrict__ yout, int strip) {
+  Col col(g);
+  const int jl0 = blockIdx.y * strip, jl1 = min(jl0 + strip, g.nyl);
+  int gj = g.j0 + jl0;
+  double xm = ldf<BC>(x, g, gj - 1, col.cc), x0 = ldf<BC>(x, g, gj, col.cc);
+  double wm = 0.0, w0 = 0.0;
+  if (KM) {
+    wm = ldf<BC_MIRROR>(op.w, g, gj - 1, col.cc);
+    w0 = ldf<BC_MIRROR>(op.w, g, gj, col.cc);
+  }
+  for (int jl = jl0; jl < jl1; ++jl, ++gj) {
+    const double xp = ldf<BC>(x, g, gj + 1, col.cc);
+    double xw = CHB_SHFL_W(x0), xe = CHB_SHFL_E(x0);
+    if (col.needW) xw = ldf<BC>(x, g, gj, col.cw);
+    if (col.needE) xe = ldf<BC>(x, g, gj, col.ce);
+    double wp = 0.0, ww = 0.0, we = 0.0;
+    if (KM) {
+      wp = ldf<BC_MIRROR>(op.w, g, gj + 1, col.cc);
+      ww = CHB_SHFL_W(w0);
+      we = CHB_SHFL_E(w0);
+      if (col.needW) ww = ldf<BC_MIRROR>(op.w, g, gj, col.cw);
+      if (col.needE) we = ldf<BC_MIRROR>(op.w, g, gj, col.ce);
+    }
+    const double ac = AM ? op.a[off(g, gj, col.cc)] : 0.0;
+    double y, d;
+    eval5T<BC, AM, KM>(op, g, gj, ac, w0, ww, we, wm, wp, x0, xw, xe, xm, xp, y, d);
+    if (col.act) yout[off(g, gj, col.c)] = y;
+    xm = x0;
+    x0 = xp;
+    wm = w0;
+    w0 = wp;
+  }
+}
+
+// ---------------------------------------------------------------- CG finish
+// x += alpha p (last iteration's update, deferred by the A kernel), or x = 0
+// when b = 0; optional reduction of sum(x) for the null-space projection.
+// mode 0: add the last alpha p; 1 (single-reduction CG, x over pairs of
+// sweeps): only after an odd iteration count; 2 (deferred p/x blocks, already
+// applied): no update, only the b = 0 case and the null-space sum.
+__global__ void __launch_bounds__(256) k_cg5_finish(Geom g, double* __restrict__ x,
+                                                    const double* __restrict__ p, int nullspace,
+                                                    int odd_only, RedArgs ra) {
+  const KScal* sc = ra.sc;
+  const int zero = sc->zero;
+  const int upd = (sc->iter >= 1) && !zero && sc->status == 0 && odd_only != 2 &&
+                  (!odd_only || (sc->iter & 1));
+  const double alpha = sc->alpha;
+  double acc = 0.0;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int jl = blockIdx.y; jl < g.nyl; jl += gridDim.y) {
+    if (c < g.nx) {
+      const size_t o = off(g, g.j0 + jl, c);
+      double v = zero ? 0.0 : x[o];
+      if (upd) v += alpha * p[o];
+      x[o] = v;
+      acc += v;
+    }
+  }
+  if (nullspace) {
+    double v[1] = {acc};
+    block_reduce_finalize<1>(v, ra);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sub_mean(Geom g, double* __restrict__ x, const KScal* sc) {
+  const double m = sc->mean;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int jl = blockIdx.y; jl < g.nyl; jl += gridDim.y)
+    if (c < g.nx) x[off(g, g.j0 + jl, c)] -= m;
+}
+
+__global__ void k_finalize_slabs(const double* tot, int nslabs, int K, RedArgs ra) {
+  // one warp (launch_finalize_slabs): lane 0 finalizes, the lanes share the
+  // coefficient-table update
+  // iteration-phase finalizers are no-ops once the solve is done (their slab
+  // kernels returned early and the totals are stale); BiCGStab's omega phase
+  // is skipped after a half-step convergence
+  const int iter_phase = ra.fin == FIN_CG_A || ra.fin == FIN_CG_B || ra.fin == FIN_CGS ||
+                         ra.fin == FIN_CGS_D0 || ra.fin == FIN_BI_ALPHA ||
+                         ra.fin == FIN_BI_S || ra.fin == FIN_BI_OMEGA || ra.fin == FIN_BI_R;
+  if (iter_phase && ra.sc->done) return;
+  if (ra.fin == FIN_BI_OMEGA && ra.sc->half) return;
+  double t[8];
+  for (int k = 0; k < K; ++k) {
+    double s = 0.0;
+    for (int i = 0; i < nslabs; ++i) s += tot[i * 8 + k];
+    t[k] = s;
+  }
+  finalize_warp(ra.fin, t, ra.sc, ra.fc);
+}
+
+// ============================================================== launchers
+static Op5T make_op(const OpDesc& d) {
+  Op5T o;
+  o.a = d.a;
+  o.w = d.w;
+  o.s = d.s;
+  o.kscale = d.kscale;
+  o.rho_n = d.rho_n;
+  o.rho_s = d.rho_s;
+  return o;
+}
+
+static dim3 grid5(const Geom& g, int strip) {
+  return dim3((g.nx + 127) / 128, (g.nyl + strip - 1) / strip);
+}
+
+#define CHB_DISPATCH(KIND, CALL)                                        \
+  switch (KIND) {                                                       \
+    case OPK_POISSON_CONST: { constexpr int BC = BC_MIRROR, AM = 0, KM = 0; CALL; } break; \
+    case OPK_POISSON_VAR:   { constexpr int BC = BC_MIRROR, AM = 0, KM = 2; CALL; } break; \
+    case OPK_NUTRIENT:      { constexpr int BC = BC_MIRROR, AM = 1, KM = 1; CALL; } break; \
+    case OPK_MOM_U:         { constexpr int BC = BC_ODD,    AM = 1, KM = 1; CALL; } break; \
+    case OPK_MOM_V:         { constexpr int BC = BC_VFACE,  AM = 1, KM = 1; CALL; } break; \
+    default: break;                                                     \
+  }
+
+void launch_cg5_init(const OpDesc& d, const Geom& g, const double* x, const double* b,
+                     int use_shift, double* z, const RedArgs& ra, cudaStream_t st) {
+  const Op5T op = make_op(d);
+  const int strip = d.strip;
+  CHB_DISPATCH(d.kind, (k_cg5_init<BC, AM, KM><<<grid5(g, strip), 128, 0, st>>>(
+                           g, op, x, b, use_shift, z, strip, ra)));
+}
+
+void launch_op5_apply(const OpDesc& d, const Geom& g, const double* x, double* y,
+                      cudaStream_t st) {
+  const Op5T op = make_op(d);
+  const int strip = d.strip;
+  CHB_DISPATCH(d.kind, (k_op5_apply<BC, AM, KM><<<grid5(g, strip), 128, 0, st>>>(g, op, x, y,
+                                                                                   strip)));
+}
+
+static dim3 grid_pw(const Geom& g) {  // ~8 CTAs per SM (bounded reduction partials)
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int gx = (g.nx + 255) / 256;
+  int gy = (nsm * 8 + gx - 1) / gx;
+  if (gy > g.nyl) gy = g.nyl;
+  if (gy < 1) gy = 1;
+  return dim3(gx, gy);
+}
+
+void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace, int odd_only,
+                       const RedArgs& ra, cudaStream_t st) {
+  k_cg5_finish<<<grid_pw(g), 256, 0, st>>>(g, x, p, nullspace, odd_only, ra);
+}
+
+void launch_sub_mean(const Geom& g, double* x, const KScal* sc, cudaStream_t st) {
+  k_sub_mean<<<grid_pw(g), 256, 0, st>>>(g, x, sc);
+}
+
+void launch_finalize_slabs(const double* tot, int nslabs, int K, const RedArgs& ra,
+                           cudaStream_t st) {
+  k_finalize_slabs<<<1, 32, 0, st>>>(tot, nslabs, K, ra);
+}
+
+}  // namespace chb

@@ -1,13 +1,9 @@
 // kernels_ch.cu -- the 13-point modified Cahn-Hilliard operator
-//   y = x^/dt + (Gamma1/2) L_{M*} Delta_h x^,   x^ = D^{-1} x (right Jacobi)
-// (Eq. 16 4th line with §4's Crank-Nicolson, R5) and
-// the BiCGStab vector updates that run around it (PAPER.md:233-244 names
-// GMRES + Jacobi; BiCGStab is the north_star's GPU choice, R14).
-//
-// The apply stages x^ (halo 2) and phi* (halo 1) in shared memory, forms
-// w = Delta_h x^ on the halo-1 tile in shared memory, then the face-mobility
-// divergence -- one HBM read of x, dinv and phi* per cell, one write of y --
-// and fuses up to two dot products into the same pass.
+//   y = x^/dt + th Gamma1 L_{M*} Delta_h x^ + ta Adv(x^; v^n),   x^ = D^{-1} x
+// (right Jacobi; Eq. 16 4th line with §4's Crank-Nicolson, th = ta
+// = 1/2, R5, R12, R23) and the BiCGStab / GMRES vector updates
+// that run around it (PAPER.md:233-244 names GMRES + Jacobi; BiCGStab is the
+// north_star's GPU choice, R14).  Even nx only (two columns per thread).
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -16,94 +12,16 @@
 
 namespace chb {
 
-constexpr int CTX = 32, CTY = 16;
-
-// periodic column (|overhang| <= 2 < nx)
-__device__ __forceinline__ int modc(int c, int nx) {
-  return c < 0 ? c + nx : (c >= nx ? c - nx : c);
-}
-
-// Mirror-fold a global row and clamp to the stored range of the slab.
-__device__ __forceinline__ int fold_row(const Geom& g, int gj) {
-  if (gj < 0) gj = -1 - gj;
-  else if (gj >= g.ny) gj = 2 * g.ny - 1 - gj;
-  int lo = g.j0 - GH, hi = g.j0 + g.nyl + GH - 1;
-  if (gj < lo) gj = lo;
-  if (gj > hi) gj = hi;
-  return gj;
-}
-
-template <int NDOT>
-__global__ void __launch_bounds__(CTX* CTY)
-    k_ch_apply(Geom g, ChCoef cc, const double* __restrict__ x, double* __restrict__ y,
-               const double* __restrict__ d1, const double* __restrict__ d2, int skip_done,
-               int skip_half, RedArgs ra) {
-  if (skip_done && ra.sc->done) return;
-  if (skip_half && ra.sc->half) return;
-  __shared__ double xs[CTY + 4][CTX + 4];
-  __shared__ double ps[CTY + 2][CTX + 2];
-  __shared__ double ws[CTY + 2][CTX + 2];
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * CTX + tx;
-  const int cx0 = blockIdx.x * CTX;
-  const int jl0 = blockIdx.y * CTY;
-  const int gj0 = g.j0 + jl0;
-  for (int idx = tid; idx < (CTY + 4) * (CTX + 4); idx += CTX * CTY) {
-    const int r = idx / (CTX + 4), c = idx % (CTX + 4);
-    const int gj = fold_row(g, gj0 + r - 2);
-    const int col = modc(cx0 + c - 2, g.nx);
-    const size_t o = off(g, gj, col);
-    double v = x[o];
-    if (cc.dinv) v *= cc.dinv[o];
-    xs[r][c] = v;
-  }
-  for (int idx = tid; idx < (CTY + 2) * (CTX + 2); idx += CTX * CTY) {
-    const int r = idx / (CTX + 2), c = idx % (CTX + 2);
-    const int gj = fold_row(g, gj0 + r - 1);
-    const int col = modc(cx0 + c - 1, g.nx);
-    ps[r][c] = cc.phis[off(g, gj, col)];
-  }
-  __syncthreads();
-  for (int idx = tid; idx < (CTY + 2) * (CTX + 2); idx += CTX * CTY) {
-    const int r = idx / (CTX + 2) + 1, c = idx % (CTX + 2) + 1;
-    ws[r - 1][c - 1] = (xs[r][c + 1] - 2.0 * xs[r][c] + xs[r][c - 1]) * g.ihx2 +
-                       (xs[r + 1][c] - 2.0 * xs[r][c] + xs[r - 1][c]) * g.ihy2;
-  }
-  __syncthreads();
-  const int gj = gj0 + ty, col = cx0 + tx;
-  double s0 = 0.0, s1 = 0.0;
-  if (jl0 + ty < g.nyl && col < g.nx) {
-    const double wc = ws[ty + 1][tx + 1];
-    const double pc = ps[ty + 1][tx + 1];
-    const double L = cc.Lambda;
-    const double mE = L * fmax(0.0, 0.5 * (pc + ps[ty + 1][tx + 2]));
-    const double mW = L * fmax(0.0, 0.5 * (pc + ps[ty + 1][tx]));
-    const double mN = (gj == g.ny - 1) ? 0.0 : L * fmax(0.0, 0.5 * (pc + ps[ty + 2][tx + 1]));
-    const double mS = (gj == 0) ? 0.0 : L * fmax(0.0, 0.5 * (pc + ps[ty][tx + 1]));
-    const double div = (mE * (ws[ty + 1][tx + 2] - wc) - mW * (wc - ws[ty + 1][tx])) * g.ihx2 +
-                       (mN * (ws[ty + 2][tx + 1] - wc) - mS * (wc - ws[ty][tx + 1])) * g.ihy2;
-    const double yv = xs[ty + 2][tx + 2] / cc.dt + cc.g1h * div;
-    const size_t o = off(g, gj, col);
-    y[o] = yv;
-    if (NDOT >= 1) s0 = yv * d1[o];
-    if (NDOT >= 2) s1 = yv * (d2 ? d2[o] : yv);
-  }
-  if (NDOT == 1) {
-    double v[1] = {s0};
-    block_reduce_finalize<1>(v, ra);
-  } else if (NDOT == 2) {
-    double v[2] = {s0, s1};
-    block_reduce_finalize<2>(v, ra);
-  }
-}
-
 // --------------------------------------------------------------------------
-// Row-marching version (default): one CTA per (<= 256-column chunk x row
-// strip), x, D^-1 and phi* rows streamed into an 8-deep shared-memory ring by
-// 1-D bulk async copies (lane 0 of warps 0-2, one array each), two columns
-// per thread, x^ = D^-1 x and w = Delta_h x^ kept in three-row register
-// windows (w recomputed on the two neighbour columns each side instead of
-// exchanged), y = x^/dt + (G1/2) L_M w one row behind.  Same arithmetic as
-// k_ch_apply.  Per cell: read x, D^-1, phi* (+ dot operands), write y.
+// Row-marching apply: one CTA per (<= 256-column chunk x row strip), x, D^-1
+// and phi* rows streamed into an 8-deep shared-memory ring by 1-D bulk async
+// copies (lane 0 of warps 0-2, one array each), two columns per thread,
+// x^ = D^-1 x and w = Delta_h x^ kept in three-row register windows (w
+// recomputed on the two neighbour columns each side instead of exchanged),
+// y = x^/dt + th G1 L_M w + ta Adv(x^) one row behind.  The face velocities
+// of the advection part (u on the cell's two x-faces, v on its two y-faces)
+// come straight from global memory at the thread's own columns.  Per cell:
+// read x, D^-1, phi* (+ u, v; + dot operands), write y.
 namespace {
 constexpr int RM_T = 128;             // threads (4 warps)
 constexpr int RM_CW = 2 * RM_T;       // max columns per chunk
@@ -201,7 +119,14 @@ __global__ void __launch_bounds__(RM_T) k_ch_rm(Geom g, ChCoef cc, const double*
     xb[j] = xh(slot(1), ci - 1 + j);
     wm[j] = wc_[j] = 0.0;
   }
-  const double L = cc.Lambda, idt = 1.0 / cc.dt;
+  const double L = cc.Lambda;
+  const bool adv = cc.u != nullptr;
+  // v on the south face of the current output row (row gj = rbase + k)
+  double2 vS2 = make_double2(0.0, 0.0);
+  if (adv && own) {
+    const int gj = rbase + 2;
+    if (gj > 0) vS2 = *reinterpret_cast<const double2*>(cc.v + off(g, gj, c0 + 2 * t));
+  }
   double s0 = 0.0, s1 = 0.0;
   for (int k = 0; k <= n + 1; ++k) {
     wait_row(k + 2);
@@ -232,10 +157,27 @@ __global__ void __launch_bounds__(RM_T) k_ch_rm(Geom g, ChCoef cc, const double*
         const double w0 = wc_[j + 1];
         const double div = (mE * (wc_[j + 2] - w0) - mW * (w0 - wc_[j])) * g.ihx2 +
                            (mN * (wp[j + 1] - w0) - mS * (w0 - wm[j + 1])) * g.ihy2;
-        yv[j] = xa[j + 1] / cc.dt + cc.g1h * div;
+        yv[j] = xa[j + 1] / cc.dt + cc.g1t * div;
       }
-      (void)idt;
       const size_t o = off(g, gj, c0 + 2 * t);
+      if (adv) {
+        // ta Adv(x^) = ta [ (uE (x+xE) - uW (xW+x)) / 2hx + (vN (x+xN) - vS (xS+x)) / 2hy ]
+        const double2 uw = *reinterpret_cast<const double2*>(cc.u + o);
+        const int ce = c0 + 2 * t + 2;
+        const double ue = cc.u[off(g, gj, ce >= g.nx ? ce - g.nx : ce)];
+        const double2 vn = gj + 1 < g.ny ? *reinterpret_cast<const double2*>(cc.v + off(g, gj + 1, c0 + 2 * t))
+                                         : make_double2(0.0, 0.0);
+        const double* xs0 = slot(k - 1);
+        const double xS0 = xh(xs0, ci), xS1 = xh(xs0, ci + 1);
+        const double hx = 0.5 * g.ihx, hy = 0.5 * g.ihy;
+        const double a0 = (uw.y * (xa[1] + xa[2]) - uw.x * (xa[0] + xa[1])) * hx +
+                          (vn.x * (xa[1] + xb[1]) - vS2.x * (xS0 + xa[1])) * hy;
+        const double a1 = (ue * (xa[2] + xa[3]) - uw.y * (xa[1] + xa[2])) * hx +
+                          (vn.y * (xa[2] + xb[2]) - vS2.y * (xS1 + xa[2])) * hy;
+        yv[0] += cc.tha * a0;
+        yv[1] += cc.tha * a1;
+        vS2 = vn;
+      }
       *reinterpret_cast<double2*>(y + o) = make_double2(yv[0], yv[1]);
       if (NDOT >= 1) {
         const double2 a = *reinterpret_cast<const double2*>(d1 + o);
@@ -293,6 +235,7 @@ void launch_rm(const Geom& g, const ChCoef& cc, const double* x, double* y, cons
   int cw = (g.nx + ncb - 1) / ncb;
   cw += cw & 1;
   long nb = (long)nsm * per_sm;
+  if (cc.strip > 0) nb = (long)ncb * ((g.nyl + cc.strip - 1) / cc.strip);  // forced strip height
   if (nb < ncb) nb = ncb;
   if (nb > (long)ncb * g.nyl) nb = (long)ncb * g.nyl;
   kern<<<(unsigned)nb, RM_T, smem, st>>>(g, cc, x, y, d1, d2, skip_done, skip_half, ncb, cw, ra);
@@ -302,26 +245,15 @@ void launch_rm(const Geom& g, const ChCoef& cc, const double* x, double* y, cons
 void launch_ch_apply(const Geom& g, const ChCoef& cc, const double* x, double* y, int ndot,
                      const double* d1, const double* d2, int skip_if_done, int skip_if_half,
                      const RedArgs& ra, cudaStream_t st) {
-  if ((g.nx % 2) == 0 && !getenv("CHB_CH_TILE")) {  // row-marching kernel (even nx)
-    if (cc.dinv) {
-      if (ndot == 0) launch_rm<0, 1>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
-      else if (ndot == 1) launch_rm<1, 1>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
-      else launch_rm<2, 1>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
-    } else {
-      if (ndot == 0) launch_rm<0, 0>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
-      else if (ndot == 1) launch_rm<1, 0>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
-      else launch_rm<2, 0>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
-    }
-    return;
+  if (cc.dinv) {
+    if (ndot == 0) launch_rm<0, 1>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
+    else if (ndot == 1) launch_rm<1, 1>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
+    else launch_rm<2, 1>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
+  } else {
+    if (ndot == 0) launch_rm<0, 0>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
+    else if (ndot == 1) launch_rm<1, 0>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
+    else launch_rm<2, 0>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra, st);
   }
-  dim3 grid((g.nx + CTX - 1) / CTX, (g.nyl + CTY - 1) / CTY);
-  dim3 block(CTX, CTY);
-  if (ndot == 0)
-    k_ch_apply<0><<<grid, block, 0, st>>>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra);
-  else if (ndot == 1)
-    k_ch_apply<1><<<grid, block, 0, st>>>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra);
-  else
-    k_ch_apply<2><<<grid, block, 0, st>>>(g, cc, x, y, d1, d2, skip_if_done, skip_if_half, ra);
 }
 
 // ------------------------------------------------------- BiCGStab updates

@@ -23,8 +23,12 @@ __device__ __forceinline__ double fprime(double p, double G2) {
   return 2.0 * G2 * p * (1.0 - p) * (1.0 - 2.0 * p);
 }
 
+// Material laws and rates take the physical volume fraction clip(phi, 0, 1) (R24).
+__device__ __forceinline__ double vfrac(double p) { return fmin(fmax(p, 0.0), 1.0); }
+
 // ------------------------------------------------------------------ CH RHS
-// b = phi/dt + L_{M*}(F'(phi*) - G1/2 Delta phi) - Adv(phi*; v^n) + g_n(phi*, c)
+// b = phi/dt + L_{M*}(F'(phi*) - (1-th) G1 Delta phi) - (1-ta) Adv(phi; v^n) + g_n(phi*, c)
+// (th = theta_ch, ta = theta_adv of this step; R5, R12, R23)
 __global__ void __launch_bounds__(256) k_ch_rhs(Geom g, Phys ph, StateP s, double* phis_out,
                                                 double* dinv, double* b) {
   CHB_CELL_PREAMBLE(g)
@@ -37,8 +41,8 @@ __global__ void __launch_bounds__(256) k_ch_rhs(Geom g, Phys ph, StateP s, doubl
     return (PHI(jj, wrapc(ii + 1, g.nx)) - 2.0 * c0 + PHI(jj, wrapc(ii - 1, g.nx))) * g.ihx2 +
            (PHI(jj + 1, ii) - 2.0 * c0 + PHI(jj - 1, ii)) * g.ihy2;
   };
-  const double g1h = 0.5 * ph.Gamma1;
-  auto MU = [&](int jj, int ii) { return fprime(PS(jj, ii), ph.Gamma2) - g1h * LAP(jj, ii); };
+  const double g1e = (1.0 - ph.th_ch) * ph.Gamma1;
+  auto MU = [&](int jj, int ii) { return fprime(PS(jj, ii), ph.Gamma2) - g1e * LAP(jj, ii); };
   const double pc = PS(j, i), pe = PS(j, ie), pw = PS(j, iw), pn = PS(j + 1, i), psv = PS(j - 1, i);
   const double L = ph.Lambda;
   const double mE = L * fmax(0.0, 0.5 * (pc + pe));
@@ -50,41 +54,44 @@ __global__ void __launch_bounds__(256) k_ch_rhs(Geom g, Phys ph, StateP s, doubl
                     (mN * (MU(j + 1, i) - muc) - mS * (muc - MU(j - 1, i))) * g.ihy2;
   const double uE = s.u[off(g, j, ie)], uW = s.u[off(g, j, i)];
   const double vN = ldf<BC_VFACE>(s.v, g, j + 1, i), vS = ldf<BC_VFACE>(s.v, g, j, i);
-  const double adv = (uE * 0.5 * (pc + pe) - uW * 0.5 * (pw + pc)) * g.ihx +
-                     (vN * 0.5 * (pc + pn) - vS * 0.5 * (psv + pc)) * g.ihy;
+  const double fc = PHI(j, i);
+  const double adv = (uE * 0.5 * (fc + PHI(j, ie)) - uW * 0.5 * (PHI(j, iw) + fc)) * g.ihx +
+                     (vN * 0.5 * (fc + PHI(j + 1, i)) - vS * 0.5 * (PHI(j - 1, i) + fc)) * g.ihy;
   const size_t o = off(g, j, i);
   const double cval = s.c[o];
-  const double grow = ph.eps * ph.mu * pc * cval / (ph.Kc + cval);
-  b[o] = s.phi[o] / ph.dt + lm - adv + grow;
+  const double grow = ph.eps * ph.mu * vfrac(pc) * cval / (ph.Kc + cval);
+  b[o] = fc / ph.dt + lm - (1.0 - ph.th_adv) * adv + grow;
   phis_out[o] = pc;
-  // Jacobi diagonal of I/dt + G1/2 L_M Delta_h (mirror walls fold onto the cell)
+  // Jacobi diagonal of I/dt + th G1 L_M Delta_h + ta Adv (mirror walls fold onto the cell)
   const double nwall = (j == 0 ? 1.0 : 0.0) + (j == g.ny - 1 ? 1.0 : 0.0);
   const double sx = (mE + mW) * g.ihx2, sy = (mN + mS) * g.ihy2;
   const double lapd = 2.0 * g.ihx2 + 2.0 * g.ihy2 - nwall * g.ihy2;
-  const double diag = 1.0 / ph.dt + g1h * ((sx + sy) * lapd + sx * g.ihx2 + sy * g.ihy2);
+  const double adiag = 0.5 * ((uE - uW) * g.ihx + (vN - vS) * g.ihy);
+  const double diag = 1.0 / ph.dt + ph.th_ch * ph.Gamma1 * ((sx + sy) * lapd + sx * g.ihx2 + sy * g.ihy2) +
+                      ph.th_adv * adiag;
   dinv[o] = 1.0 / diag;
 }
 
 // ------------------------------------------------------------ nutrient RHS
-// a = phi_s^{n+1}/dt + A/2 phi^{1/2};  w = phi_s^{1/2};
+// a = phi_s^{n+1}/dt + A/2 phi^{1/2};  w = phi_s^{1/2};  volume fractions clipped (R24)
 // b = phi_s^n c/dt - Adv(phi_s^n c) + 1/2 L_K c - A/2 phi^{1/2} c,  K = Ds * face mean(w)
 __global__ void __launch_bounds__(256) k_nut_rhs(Geom g, Phys ph, StateP s,
                                                  const double* __restrict__ phi1, double* a,
                                                  double* w, double* b) {
   CHB_CELL_PREAMBLE(g)
   auto SH = [&](int jj, int ii) {
-    return 1.0 - 0.5 * (ldf<BC_MIRROR>(s.phi, g, jj, ii) + ldf<BC_MIRROR>(phi1, g, jj, ii));
+    return 1.0 - vfrac(0.5 * (ldf<BC_MIRROR>(s.phi, g, jj, ii) + ldf<BC_MIRROR>(phi1, g, jj, ii)));
   };
   auto W = [&](int jj, int ii) {
-    return (1.0 - ldf<BC_MIRROR>(s.phi, g, jj, ii)) * ldf<BC_MIRROR>(s.c, g, jj, ii);
+    return (1.0 - vfrac(ldf<BC_MIRROR>(s.phi, g, jj, ii))) * ldf<BC_MIRROR>(s.c, g, jj, ii);
   };
   auto C = [&](int jj, int ii) { return ldf<BC_MIRROR>(s.c, g, jj, ii); };
   const size_t o = off(g, j, i);
   const double phin = s.phi[o], p1 = phi1[o];
-  const double phalf = 0.5 * (phin + p1);
+  const double phalf = vfrac(0.5 * (phin + p1));
   const double sh = 1.0 - phalf;
   const double cc = s.c[o];
-  a[o] = (1.0 - p1) / ph.dt + 0.5 * ph.A * phalf;
+  a[o] = (1.0 - vfrac(p1)) / ph.dt + 0.5 * ph.A * phalf;
   w[o] = sh;
   const double wc = W(j, i), we = W(j, ie), ww = W(j, iw), wn = W(j + 1, i), ws = W(j - 1, i);
   const double uE = s.u[off(g, j, ie)], uW = s.u[off(g, j, i)];
@@ -99,10 +106,14 @@ __global__ void __launch_bounds__(256) k_nut_rhs(Geom g, Phys ph, StateP s,
 }
 
 // -------------------------------------------------------- momentum pieces
-__device__ __forceinline__ void visc(const Phys& ph, double f, double& rho, double& nu) {
-  rho = ph.rho_s + f * (ph.rho_n - ph.rho_s);
-  const double eta = f / ph.Re_n + (1.0 - f) / ph.Re_s;
-  nu = eta / rho;
+// Mixture density and viscosity eta = 1/Re_a = f/Re_n + (1-f)/Re_s of the
+// volume fraction f = clip(phi, 0, 1) (Eq. 15, R6, R24).
+__device__ __forceinline__ double dens(const Phys& ph, double phi) {
+  return ph.rho_s + vfrac(phi) * (ph.rho_n - ph.rho_s);
+}
+__device__ __forceinline__ double visc_eta(const Phys& ph, double phi) {
+  const double f = vfrac(phi);
+  return f / ph.Re_n + (1.0 - f) / ph.Re_s;
 }
 
 struct PhiStar {
@@ -125,63 +136,101 @@ struct PhiStar {
     const double d = ((*this)(jj + 1, ii) - (*this)(jj - 1, ii)) * 0.5 * g.ihy;
     return d * d;
   }
+  // phi at the u point (x-face) (jj, ii), at the v point (y-face) (jj, ii), at a corner
+  __device__ __forceinline__ double fu(int jj, int ii) const {
+    return 0.5 * ((*this)(jj, ii - 1) + (*this)(jj, ii));
+  }
+  __device__ __forceinline__ double fv(int jj, int ii) const {
+    return 0.5 * ((*this)(jj - 1, ii) + (*this)(jj, ii));
+  }
+  __device__ __forceinline__ double fk(int jj, int ii) const {
+    return 0.25 * ((*this)(jj, ii) + (*this)(jj, ii - 1) + (*this)(jj - 1, ii) +
+                   (*this)(jj - 1, ii - 1));
+  }
 };
 
-// u on x-faces: a = 1/(nu dt);  b = a u + 1/2 Lap u + lid + (-C_u + R_x/rho)/nu
+// u on x-faces (R6, R7; th = theta_visc, 1 = the viscous term at u^{n+1}, Eq. 19):
+//   a = rho/dt, w = eta at the u point,
+//   b = a u + (1-th) div(eta grad u) + th lid - rho (v.grad)u + R_x,
+//   R = -G1 div(grad phi* grad phi*) + div(eta (grad v)^T)       (Eq. 17)
 __global__ void __launch_bounds__(256) k_mom_rhs_u(Geom g, Phys ph, StateP s,
                                                    const double* __restrict__ phis, double* a,
-                                                   double* b) {
+                                                   double* w, double* b) {
   CHB_CELL_PREAMBLE(g)
   PhiStar P{phis, g};
-  const double f = 0.5 * (P(j, i - 1) + P(j, i));
-  double rho, nu;
-  visc(ph, f, rho, nu);
-  const double ac = 1.0 / (nu * ph.dt);
+  const double rho = dens(ph, P.fu(j, i));
+  const double ec = visc_eta(ph, P.fu(j, i));
   const double Rx = -ph.Gamma1 * ((P.txx(j, i) - P.txx(j, i - 1)) * g.ihx +
                                   (P.txy(j + 1, i) - P.txy(j, i)) * g.ihy);
   auto U = [&](int jj, int ii) { return ld_u_lid(s.u, g, jj, ii, ph.lid_u); };
-  auto V = [&](int jj, int ii) { return ldf<BC_VFACE>(s.v, g, jj, ii); };
+  auto V = [&](int jj, int ii) { return ldf<BC_VFACE>(s.v, g, jj, wrapc(ii, g.nx)); };
   const size_t o = off(g, j, i);
   const double uc = s.u[o];
   const double vbar = 0.25 * (V(j, iw) + V(j, i) + V(j + 1, iw) + V(j + 1, i));
   const double cu = uc * (U(j, ie) - U(j, iw)) * 0.5 * g.ihx +
                     vbar * (U(j + 1, i) - U(j - 1, i)) * 0.5 * g.ihy;
-  const double lap = (U(j, ie) - 2.0 * uc + U(j, iw)) * g.ihx2 +
-                     (U(j + 1, i) - 2.0 * uc + U(j - 1, i)) * g.ihy2;
-  double rhs = ac * uc + 0.5 * lap + (-cu + Rx / rho) / nu;
-  if (j == g.ny - 1) rhs += ph.lid_u * g.ihy2;
+  // div(eta grad u): face coefficient = mean of eta at the two u points; the
+  // coefficient's wall ghost is its mirror image (PhiStar's mirror rows)
+  const double kE = 0.5 * (ec + visc_eta(ph, P.fu(j, ie))), kW = 0.5 * (ec + visc_eta(ph, P.fu(j, iw)));
+  const double kN = 0.5 * (ec + visc_eta(ph, P.fu(j + 1, i)));
+  const double kS = 0.5 * (ec + visc_eta(ph, P.fu(j - 1, i)));
+  const double lap = (kE * (U(j, ie) - uc) - kW * (uc - U(j, iw))) * g.ihx2 +
+                     (kN * (U(j + 1, i) - uc) - kS * (uc - U(j - 1, i))) * g.ihy2;
+  // div(eta (grad v)^T): eta du/dx at the cells left/right, eta dv/dx at the corners below/above
+  const double qR = visc_eta(ph, P(j, i)) * (U(j, ie) - uc) * g.ihx;
+  const double qL = visc_eta(ph, P(j, i - 1)) * (uc - U(j, iw)) * g.ihx;
+  const double rN = visc_eta(ph, P.fk(j + 1, i)) * (V(j + 1, i) - V(j + 1, i - 1)) * g.ihx;
+  const double rS = visc_eta(ph, P.fk(j, i)) * (V(j, i) - V(j, i - 1)) * g.ihx;
+  const double Tx = (qR - qL) * g.ihx + (rN - rS) * g.ihy;
+  const double ac = rho / ph.dt;
+  double rhs = ac * uc + (1.0 - ph.th_visc) * lap - rho * cu + Rx + Tx;
+  if (j == g.ny - 1) rhs += ph.th_visc * kN * 2.0 * ph.lid_u * g.ihy2;
   a[o] = ac;
+  w[o] = ec;
   b[o] = rhs;
 }
 
-// v on y-faces j >= 1 (row 0 = wall: identity row, b = 0)
+// v on y-faces j >= 1 (row 0 = wall: identity row, b = 0; its w = eta(phi[0]) is
+// the coefficient source of the face between rows 0 and 1)
 __global__ void __launch_bounds__(256) k_mom_rhs_v(Geom g, Phys ph, StateP s,
                                                    const double* __restrict__ phis, double* a,
-                                                   double* b) {
+                                                   double* w, double* b) {
   CHB_CELL_PREAMBLE(g)
+  PhiStar P{phis, g};
   const size_t o = off(g, j, i);
   if (j == 0) {
     a[o] = 1.0;
+    w[o] = visc_eta(ph, P(0, i));
     b[o] = 0.0;
     return;
   }
-  PhiStar P{phis, g};
-  const double f = 0.5 * (P(j - 1, i) + P(j, i));
-  double rho, nu;
-  visc(ph, f, rho, nu);
-  const double ac = 1.0 / (nu * ph.dt);
+  const double rho = dens(ph, P.fv(j, i));
+  const double ec = visc_eta(ph, P.fv(j, i));
   const double Ry = -ph.Gamma1 * ((P.txy(j, i + 1) - P.txy(j, i)) * g.ihx +
                                   (P.tyy(j, i) - P.tyy(j - 1, i)) * g.ihy);
   auto V = [&](int jj, int ii) { return ldf<BC_VFACE>(s.v, g, jj, ii); };
+  auto Uc = [&](int jj, int ii) { return s.u[off(g, jj, ii)]; };
   const double vc = s.v[o];
-  const double ubar = 0.25 * (s.u[off(g, j - 1, i)] + s.u[off(g, j - 1, ie)] + s.u[off(g, j, i)] +
-                              s.u[off(g, j, ie)]);
+  const double ubar = 0.25 * (Uc(j - 1, i) + Uc(j - 1, ie) + Uc(j, i) + Uc(j, ie));
   const double cv = ubar * (V(j, ie) - V(j, iw)) * 0.5 * g.ihx +
                     vc * (V(j + 1, i) - V(j - 1, i)) * 0.5 * g.ihy;
-  const double lap = (V(j, ie) - 2.0 * vc + V(j, iw)) * g.ihx2 +
-                     (V(j + 1, i) - 2.0 * vc + V(j - 1, i)) * g.ihy2;
+  const double kE = 0.5 * (ec + visc_eta(ph, P.fv(j, ie))), kW = 0.5 * (ec + visc_eta(ph, P.fv(j, iw)));
+  // eta at the v point below (row 0: eta(phi[0])), above (top ghost: the mirror, eta itself)
+  const double eS = j == 1 ? visc_eta(ph, P(0, i)) : visc_eta(ph, P.fv(j - 1, i));
+  const double eN = j == g.ny - 1 ? ec : visc_eta(ph, P.fv(j + 1, i));
+  const double kN = 0.5 * (ec + eN), kS = 0.5 * (ec + eS);
+  const double lap = (kE * (V(j, ie) - vc) - kW * (vc - V(j, iw))) * g.ihx2 +
+                     (kN * (V(j + 1, i) - vc) - kS * (vc - V(j - 1, i))) * g.ihy2;
+  // div(eta (grad v)^T): eta du/dy at the corners left/right, eta dv/dy at the cells below/above
+  const double qR = visc_eta(ph, P.fk(j, i + 1)) * (Uc(j, ie) - Uc(j - 1, ie)) * g.ihy;
+  const double qL = visc_eta(ph, P.fk(j, i)) * (Uc(j, i) - Uc(j - 1, i)) * g.ihy;
+  const double rN = visc_eta(ph, P(j, i)) * (V(j + 1, i) - vc) * g.ihy;
+  const double rS = visc_eta(ph, P(j - 1, i)) * (vc - V(j - 1, i)) * g.ihy;
+  const double Ty = (qR - qL) * g.ihx + (rN - rS) * g.ihy;
+  const double ac = rho / ph.dt;
   a[o] = ac;
-  b[o] = ac * vc + 0.5 * lap + (-cv + Ry / rho) / nu;
+  w[o] = ec;
+  b[o] = ac * vc + (1.0 - ph.th_visc) * lap - rho * cv + Ry + Ty;
 }
 
 // ---------------------------------------------------------- projection
@@ -216,13 +265,13 @@ __global__ void __launch_bounds__(256) k_project(Geom g, Phys ph, const double* 
   CHB_CELL_PREAMBLE(g)
   (void)ie;
   const size_t o = off(g, j, i);
-  const double fu = 0.5 * (phi1[off(g, j, iw)] + phi1[o]);
+  const double fu = vfrac(0.5 * (phi1[off(g, j, iw)] + phi1[o]));
   const double bu = 1.0 / (ph.rho_s + fu * (ph.rho_n - ph.rho_s));
   u[o] = us[o] + bu * (p[o] - p[off(g, j, iw)]) * g.ihx;
   if (j == 0) {
     v[o] = 0.0;
   } else {
-    const double fv = 0.5 * (phi1[off(g, j - 1, i)] + phi1[o]);
+    const double fv = vfrac(0.5 * (phi1[off(g, j - 1, i)] + phi1[o]));
     const double bv = 1.0 / (ph.rho_s + fv * (ph.rho_n - ph.rho_s));
     v[o] = vs[o] + bv * (p[o] - p[off(g, j - 1, i)]) * g.ihy;
   }
@@ -237,12 +286,12 @@ void launch_nut_rhs(const Geom& g, const Phys& ph, StateP s, const double* phi1,
   k_nut_rhs<<<grid2(g), blk2, 0, st>>>(g, ph, s, phi1, a, w, b);
 }
 void launch_mom_rhs_u(const Geom& g, const Phys& ph, StateP s, const double* phis, double* a,
-                      double* b, cudaStream_t st) {
-  k_mom_rhs_u<<<grid2(g), blk2, 0, st>>>(g, ph, s, phis, a, b);
+                      double* w, double* b, cudaStream_t st) {
+  k_mom_rhs_u<<<grid2(g), blk2, 0, st>>>(g, ph, s, phis, a, w, b);
 }
 void launch_mom_rhs_v(const Geom& g, const Phys& ph, StateP s, const double* phis, double* a,
-                      double* b, cudaStream_t st) {
-  k_mom_rhs_v<<<grid2(g), blk2, 0, st>>>(g, ph, s, phis, a, b);
+                      double* w, double* b, cudaStream_t st) {
+  k_mom_rhs_v<<<grid2(g), blk2, 0, st>>>(g, ph, s, phis, a, w, b);
 }
 void launch_div(const Geom& g, const double* us, const double* vs, double* b, const RedArgs& ra,
                 cudaStream_t st) {

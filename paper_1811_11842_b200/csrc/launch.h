@@ -14,47 +14,19 @@ enum OpKind : int {
   OPK_MOM_V = 4
 };
 
-// Operator descriptor for the 5-point family (see kernels_cg5.cu).
+// Operator descriptor for the 5-point family (op5.cuh, kernels_aux.cu, kernels_cgs.cu).
 struct OpDesc {
   int kind;
-  int strip;          // rows per marching strip (scalar kernels)
-  int strip2;         // rows per strip of the vectorised kernels
-  int vec;            // use the 2-column vectorised kernels when nx is even
+  int strip;          // rows per marching strip (column-marching kernels)
+  int strip2;         // rows per strip of the fused CG sweep (0 = one resident wave)
   int pdl;            // programmatic dependent launch for the fused CG sweeps
   const double* a;    // diagonal coefficient array (NUTRIENT, MOM_*)
   const double* w;    // cell coefficient (NUTRIENT: phi_s^{1/2}; POISSON_VAR: phi^{n+1})
   double s, kscale, rho_n, rho_s;
 };
 
-// Algorithmic bytes per cell of the fused CG kernels.
-inline double cg5_bytes_A(int kind) {
-  switch (kind) {
-    case OPK_POISSON_CONST: return 40.0;
-    case OPK_POISSON_VAR: return 48.0;
-    case OPK_NUTRIENT: return 56.0;
-    default: return 48.0;
-  }
-}
-inline double cg5_bytes_B(int kind) {
-  switch (kind) {
-    case OPK_POISSON_CONST: return 24.0;
-    case OPK_POISSON_VAR: return 32.0;
-    case OPK_NUTRIENT: return 40.0;
-    default: return 32.0;
-  }
-}
-
 void launch_cg5_init(const OpDesc& d, const Geom& g, const double* x, const double* b,
                      int use_shift, double* z, const RedArgs& ra, cudaStream_t st);
-void launch_cg5_A(const OpDesc& d, const Geom& g, const double* z, const double* po, double* pn,
-                  double* x, int first, const RedArgs& ra, cudaStream_t st);
-void launch_cg5_B(const OpDesc& d, const Geom& g, const double* p, double* z, const RedArgs& ra,
-                  cudaStream_t st);
-// TMA-staged variants (kernels_cg5_tma.cu), even nx only
-void launch_cg5_A_tma(const OpDesc& d, const Geom& g, const double* z, const double* po,
-                      double* pn, double* x, int first, const RedArgs& ra, cudaStream_t st);
-void launch_cg5_B_tma(const OpDesc& d, const Geom& g, const double* p, double* z,
-                      const RedArgs& ra, cudaStream_t st);
 void launch_op5_apply(const OpDesc& d, const Geom& g, const double* x, double* y,
                       cudaStream_t st);
 void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace, int odd_only,
@@ -97,7 +69,11 @@ void launch_finalize_slabs(const double* tot, int nslabs, int K, const RedArgs& 
 struct ChCoef {
   const double* phis;  // phi* (mobility source)
   const double* dinv;  // Jacobi inverse diagonal (nullptr: no scaling)
-  double dt, g1h, Lambda;  // g1h = Gamma1 / 2
+  const double* u;     // face velocities v^n of the implicit advection part
+  const double* v;     //   (u == nullptr: no advection part)
+  double dt, g1t, Lambda;  // g1t = theta_ch * Gamma1
+  double tha;              // theta_adv
+  int strip;               // forced rows per strip (0: one resident wave; env CHB_STRIP)
 };
 // y = A (dinv .* x)  [or A x when dinv == nullptr]; fused dots:
 //   ndot = 0: none; 1: (y, d1); 2: (y, d1), (y, d2) where d2 == nullptr means (y, y)
@@ -129,6 +105,7 @@ void launch_gm_update_x(const Geom& g, double* const* V, int k, const double* co
 // ---- explicit right-hand sides and projection (kernels_rhs.cu)
 struct Phys {
   double dt, Gamma1, Gamma2, Lambda, mu, Kc, eps, A, Ds, Re_s, Re_n, rho_n, rho_s, lid_u;
+  double th_ch, th_adv, th_visc;  // implicit weights of this step (R5, R12, R7, R23)
 };
 struct StateP {
   const double *phi, *phip, *c, *u, *v, *p;
@@ -138,15 +115,12 @@ void launch_ch_rhs(const Geom& g, const Phys& ph, StateP s, double* phis, double
 void launch_nut_rhs(const Geom& g, const Phys& ph, StateP s, const double* phi1, double* a,
                     double* w, double* b, cudaStream_t st);
 void launch_mom_rhs_u(const Geom& g, const Phys& ph, StateP s, const double* phis, double* a,
-                      double* b, cudaStream_t st);
+                      double* w, double* b, cudaStream_t st);
 void launch_mom_rhs_v(const Geom& g, const Phys& ph, StateP s, const double* phis, double* a,
-                      double* b, cudaStream_t st);
-void launch_mom_coef(const Geom& g, const Phys& ph, const double* phis, double* au, double* av,
-                     cudaStream_t st);
+                      double* w, double* b, cudaStream_t st);
 void launch_div(const Geom& g, const double* us, const double* vs, double* b, const RedArgs& ra,
                 cudaStream_t st);
 void launch_project(const Geom& g, const Phys& ph, const double* phi1, const double* us,
                     const double* vs, const double* p, double* u, double* v, cudaStream_t st);
-void launch_copy_rows(const Geom& g, const double* src, double* dst, cudaStream_t st);
 
 }  // namespace chb

@@ -18,7 +18,8 @@ __device__ __forceinline__ double kfaceT(const Op5T& op, double w1, double w2) {
   if (KM == 0) return 1.0;
   const double m = 0.5 * (w1 + w2);
   if (KM == 1) return op.kscale * m;
-  return 1.0 / (op.rho_s + m * (op.rho_n - op.rho_s));
+  const double f = fmin(fmax(m, 0.0), 1.0);   // volume fraction (R24)
+  return 1.0 / (op.rho_s + f * (op.rho_n - op.rho_s));
 }
 
 template <int BC, int AM, int KM>

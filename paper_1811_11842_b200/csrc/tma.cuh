@@ -71,45 +71,3 @@ __device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 }  // namespace chb
-
-namespace chb {
-// Bulk prefetch of a global range into L2 (no shared memory, no completion
-// tracking): lets a shallow shared-memory ring run far ahead of HBM latency.
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-}  // namespace chb
-
-// ---- L2 eviction-priority hints (createpolicy + .L2::cache_hint)
-namespace chb {
-__device__ __forceinline__ uint64_t l2_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t l2_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void bulk_g2s_s_hint(uint32_t dst, const void* src, uint32_t bytes,
-                                                uint32_t bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void st_v2_hint(double* p, double x, double y, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(x), "d"(y),
-               "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ double2 ldg_v2_hint(const double* p, uint64_t pol) {
-  double2 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-               : "=d"(v.x), "=d"(v.y)
-               : "l"(p), "l"(pol));
-  return v;
-}
-}  // namespace chb

@@ -25,7 +25,19 @@ def test_reference_arm_line():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
-    assert d["config"]["workload"].startswith("64x64")
+    # whole oracle steps at configs[1]'s grid: the timed region is what ran
+    assert d["config"]["workload"].startswith("256x256")
+    assert d["ms_per_step"] * d["steps"] < 60e3
+
+
+def test_default_run_is_the_declared_workload():
+    """No flags = BASELINE configs[3] for its declared 20 steps after 5 warm-up."""
+    sys.path.insert(0, ROOT)
+    import bench
+    a = bench.parse_args([])
+    assert (a.config, a.steps, a.warmup, a.gpus) == (3, 20, 5, 1)
+    assert bench.CONFIGS[a.config]["name"] == "4096x4096_20steps"
+    assert bench.parse_args(["--config", "2"]).steps == 50
 
 
 @pytest.mark.gpu

@@ -95,14 +95,38 @@ def test_assembled_matches_bruteforce(nx, ny):
     Mx, My = ex.mobility_faces(phis, prm.Lambda)
     A = asm.ch_matrix(nx, ny, prm.dt, prm.Gamma1, Mx, My)
     assert _rel(A @ x.ravel(), brute.ch_apply(phis, x, prm.dt, prm.Gamma1, prm.Lambda)) < 1e-13
+    uu = rng.standard_normal((ny, nx))
+    vv = rng.standard_normal((ny, nx))
+    vv[0] = 0.0
+    A = asm.ch_matrix(nx, ny, prm.dt, prm.Gamma1, Mx, My, 0.7, 0.4, uu, vv)
+    assert _rel(A @ x.ravel(), brute.ch_apply(phis, x, prm.dt, prm.Gamma1, prm.Lambda,
+                                              0.7, 0.4, uu, vv)) < 1e-13
     bx, by = ex.pressure_faces(phis, 2.0, 1.0)
     assert _rel(asm.poisson_matrix(nx, ny, bx, by) @ x.ravel(),
                 brute.poisson_apply(phis, x, 2.0, 1.0)) < 1e-13
     a = 1.0 + rng.random((ny, nx))
-    assert _rel(asm.u_matrix(nx, ny, a) @ x.ravel(), brute.u_apply(a, x)) < 1e-13
-    xv = x.copy()
-    xv[0] = 0.0
-    assert _rel(asm.v_matrix(nx, ny, a) @ xv.ravel(), brute.v_apply(a, xv)) < 1e-13
+    eta = 0.5 + rng.random((ny, nx))
+    K = ex.node_fluxes(eta)
+    for th in (1.0, 0.5):
+        assert _rel(asm.u_matrix(nx, ny, a, K, th) @ x.ravel(), brute.u_apply(a, eta, x, th)) < 1e-13
+        xv = x.copy()
+        xv[0] = 0.0
+        assert _rel(asm.v_matrix(nx, ny, a, K, th) @ xv.ravel(),
+                    brute.v_apply(a, eta, xv, th)) < 1e-13
+    # the explicit parts of the momentum right-hand side
+    ue = rng.standard_normal((ny, nx))
+    ve = rng.standard_normal((ny, nx))
+    ve[0] = 0.0
+    phv = rng.uniform(-0.1, 1.1, (ny, nx))   # exercises the volume-fraction clip (R24)
+    tx, ty = brute.visc_transpose(ue, ve, phv, 0.3, 2.0)
+    Tx, Ty = ex.visc_transpose(ue, ve, phv, 0.3, 2.0)
+    assert _rel(Tx, tx) < 1e-13 and _rel(Ty, ty) < 1e-13
+    lid = 0.7
+    assert _rel(ex.visc_u_inhom(ue, eta, 0.0), -brute.u_apply(np.zeros_like(a), eta, ue)) < 1e-13
+    assert _rel(ex.visc_v(ve, eta)[1:], -brute.v_apply(np.zeros_like(a), eta, ve)[1:]) < 1e-13
+    lidpart = ex.visc_u_inhom(ue, eta, lid) - ex.visc_u_inhom(ue, eta, 0.0)
+    assert np.abs(lidpart[:-1]).max() < 1e-9
+    assert _rel(lidpart[-1], 2 * lid * eta[-1] * ny * ny) < 1e-13
     u = rng.standard_normal((ny, nx))
     v = rng.standard_normal((ny, nx))
     v[0] = 0.0
@@ -168,7 +192,7 @@ def test_ch_step_closed_form_amplification():
     e = np.cos(2 * np.pi * k * X) * np.cos(np.pi * l * Y)
     lam = -(4 * nx * nx) * np.sin(np.pi * k / nx) ** 2 - (4 * ny * ny) * np.sin(np.pi * l / (2 * ny)) ** 2
     phi0, d = 0.3, 1e-3
-    prm = Params(Lambda=0.1, eps=0.0, rtol=1e-14)
+    prm = Params(Lambda=0.1, eps=0.0, rtol=1e-14, startup_be=0)
     z = np.zeros((ny, nx))
     st = State(phi=phi0 + d * e, phi_prev=phi0 + 3 * d * e, c=np.ones((ny, nx)), u=z, v=z, p=z)
     A, b, phs = ch_system(st, prm)
@@ -201,8 +225,10 @@ def test_nutrient_step_closed_form():
 
 def test_momentum_shear_mode_closed_form_full_step():
     """x-independent shear mode u = d sin(pi l y), v = 0, uniform phi, lid 0:
-    convection and R vanish, D u* = 0 so p = 0, and the full step multiplies
-    the mode by (a + lam/2)/(a - lam/2), a = 1/(nu dt)."""
+    convection and R (incl. its viscous part) vanish, D u* = 0 so p = 0, and
+    the full step multiplies the mode by (a + (1-th) lam)/(a - th lam),
+    a = rho/(eta dt): a/(a - lam) for the implicit viscous term of Eq. 19
+    (th = 1, R7), (a + lam/2)/(a - lam/2) for Crank-Nicolson."""
     nx, ny = 8, 16
     X, Y = _grid(nx, ny)
     l = 1
@@ -214,12 +240,13 @@ def test_momentum_shear_mode_closed_form_full_step():
     a = 1 / (nu * prm.dt)
     z = np.zeros((ny, nx))
     d = 0.1
-    st = State(phi=np.full((ny, nx), phi0), phi_prev=np.full((ny, nx), phi0),
-               c=np.ones((ny, nx)), u=d * e, v=z.copy(), p=z.copy())
-    new, info = step(st, prm)
-    assert _rel(new.u, d * e * (a + lam / 2) / (a - lam / 2)) < 1e-12
-    assert np.abs(new.v).max() < 1e-14 and np.abs(new.p).max() < 1e-14
-    assert np.abs(new.phi - phi0).max() < 1e-14
+    for th in (1.0, 0.5):
+        st = State(phi=np.full((ny, nx), phi0), phi_prev=np.full((ny, nx), phi0),
+                   c=np.ones((ny, nx)), u=d * e, v=z.copy(), p=z.copy())
+        new, info = step(st, prm.with_(theta_visc=th))
+        assert _rel(new.u, d * e * (a + (1 - th) * lam) / (a - th * lam)) < 1e-12
+        assert np.abs(new.v).max() < 1e-14 and np.abs(new.p).max() < 1e-14
+        assert np.abs(new.phi - phi0).max() < 1e-14
 
 
 def test_couette_is_exact_steady_state():
@@ -301,7 +328,7 @@ def test_ch_step_time_order_two():
     e = np.cos(2 * np.pi * X) * np.cos(np.pi * Y)
     lam = -(4 * nx * nx) * np.sin(np.pi / nx) ** 2 - (4 * ny * ny) * np.sin(np.pi / (2 * ny)) ** 2
     phi0, d, T = 0.3, 1e-3, 0.2
-    prm0 = Params(Lambda=1e-4, eps=0.0, rtol=1e-14)
+    prm0 = Params(Lambda=1e-4, eps=0.0, rtol=1e-14, startup_be=0)
     sigma = 0.5 * prm0.Gamma1 * prm0.Lambda * phi0 * lam ** 2 * 2   # d/dt amp = -G1 L phi0 lam^2 amp
     errs = []
     for dt in (2e-3, 1e-3, 5e-4):
@@ -365,7 +392,7 @@ def test_free_energy_decays_pure_ch():
     for _ in range(150):
         A, b, phs = ch_system(st, prm)
         x, _ = bicgstab(A, b, phs.ravel(), 1 / A.diagonal(), prm.rtol, 5000)
-        st = State(phi=x.reshape(n, n), phi_prev=st.phi, c=st.c, u=z, v=z, p=z)
+        st = State(phi=x.reshape(n, n), phi_prev=st.phi, c=st.c, u=z, v=z, p=z, n=st.n + 1)
         E.append(ex.free_energy(st.phi, prm.Gamma1, prm.Gamma2))
     E = np.array(E)
     assert np.all(np.diff(E[5:]) <= 1e-12 * E[0]), np.diff(E[5:]).max()
@@ -448,14 +475,276 @@ def test_stratified_phase_stress_is_balanced_by_pressure():
     gy[-1] = (prof[-1] - prof[-2]) / (2 * h)
     Tyy = gy ** 2
     Ry = -prm.Gamma1 * (Tyy[1:] - Tyy[:-1]) / h           # faces j = 1..ny-1
-    fphi = 0.5 * (prof[1:] + prof[:-1])
-    nu = fphi / prm.Re_n + (1 - fphi) / prm.Re_s
-    a = 1 / (nu * prm.dt)
-    m = ny - 1
-    M = np.diag(a + 1 / h ** 2) - np.diag(np.full(m - 1, 0.5 / h ** 2), 1) - np.diag(np.full(m - 1, 0.5 / h ** 2), -1)
-    vstar = np.linalg.solve(M, Ry / nu)
+    # implicit viscous operator rho/dt - d/dy(eta d/dy) on the v points j = 1..ny-1
+    # (v = 0 on both walls), eta at the v points from the face mean of phi
+    # (row 0: the wall, phi[0]), face coefficients = mean of the two (R6)
+    fphi = np.concatenate([[prof[0]], 0.5 * (prof[1:] + prof[:-1])])
+    eta = fphi / prm.Re_n + (1 - fphi) / prm.Re_s
+    etap = np.concatenate([eta, [eta[-1]]])           # mirror ghost above the top point
+    KS = 0.5 * (eta[:-1] + eta[1:])                   # between points j-1 and j, j = 1..ny-1
+    KN = 0.5 * (eta[1:] + etap[2:])                   # between j and j+1
+    M = (np.diag(1 / prm.dt + (KS + KN) / h ** 2) - np.diag(KN[:-1] / h ** 2, 1)
+         - np.diag(KS[1:] / h ** 2, -1))
+    vstar = np.linalg.solve(M, Ry)
     p = np.concatenate([[0.0], np.cumsum(-vstar * h)])    # beta = 1 (rho_n = rho_s)
     p -= p.mean()
     assert np.abs(p).max() > 1e-6
     assert _rel(new.p[:, 0], p) < 1e-9
     assert np.abs(new.p - new.p[:, :1]).max() < 1e-12
+
+
+# ------------------------------------------------- implicit advection (R12)
+def _streamfunction_velocity(nx, ny, seed):
+    """Discretely divergence-free MAC velocity from a random corner stream
+    function psi with psi = 0 on both walls: u = d psi/dy on x-faces,
+    v = -d psi/dx on y-faces (so D_h(u, v) = 0 exactly and v = 0 on the walls)."""
+    rng = np.random.default_rng(seed)
+    psi = rng.standard_normal((ny + 1, nx))
+    psi[0] = psi[-1] = 0.0
+    u = (psi[1:] - psi[:-1]) * ny
+    v = -(np.roll(psi, -1, axis=1) - psi)[:ny] * nx
+    return u, v
+
+
+def test_advection_matrix_structure():
+    """Central conservative fluxes: A + A^T = diag(D_h v) (skew-symmetric for a
+    discretely divergence-free v), A 1 = D_h v, and the column sums vanish
+    (telescoping fluxes, zero wall flux)."""
+    nx, ny = 7, 6
+    rng = np.random.default_rng(4)
+    u = rng.standard_normal((ny, nx))
+    v = rng.standard_normal((ny, nx))
+    v[0] = 0.0
+    A = asm.advection_matrix(nx, ny, u, v)
+    div = ex.divergence(u, v).ravel()
+    assert abs(A + A.T - sp.diags(div)).max() < 1e-12 * nx
+    assert np.abs(A @ np.ones(nx * ny) - div).max() < 1e-12 * nx
+    assert np.abs(np.ones(nx * ny) @ A).max() < 1e-12 * nx
+    us, vs = _streamfunction_velocity(nx, ny, 1)
+    assert np.abs(ex.divergence(us, vs)).max() < 1e-12 * nx * ny
+    B = asm.advection_matrix(nx, ny, us, vs)
+    assert abs(B + B.T).max() < 1e-11 * nx * ny
+
+
+@pytest.mark.parametrize("startup", [0, 1])
+def test_ch_advection_translation_closed_form(startup):
+    """Pure translation u = U, v = 0, no CH flux (Lambda = 0), no production:
+    the x-mode cos(2 pi k x) is an eigenvector of the central advection with
+    eigenvalue i U sin(2 pi k h)/h, so one CH step multiplies its complex
+    amplitude by (1 - (1-ta) dt i s)/(1 + ta dt i s), ta = 1/2 (CN, R12) or 1
+    in a backward-Euler start-up step (R23)."""
+    nx, ny = 16, 6
+    X, Y = _grid(nx, ny)
+    k, U, d, phi0 = 3, 2.0, 1e-2, 0.3
+    prm = Params(Lambda=0.0, eps=0.0, dt=0.02, startup_be=startup)
+    z = np.zeros((ny, nx))
+    phi = phi0 + d * np.cos(2 * np.pi * k * X)
+    st = State(phi=phi, phi_prev=phi.copy(), c=np.ones((ny, nx)), u=np.full((ny, nx), U),
+               v=z, p=z)
+    A, b, phs = ch_system(st, prm)
+    x, _ = bicgstab(A, b, phs.ravel(), 1 / A.diagonal(), 1e-14, 1000)
+    ta = 1.0 if startup else 0.5
+    s = U * math.sin(2 * np.pi * k / nx) * nx
+    g = (1 - (1 - ta) * prm.dt * 1j * s) / (1 + ta * prm.dt * 1j * s)
+    assert abs(g) < 1 if startup else abs(abs(g) - 1) < 1e-15
+    exact = phi0 + d * np.real(g * np.exp(2j * np.pi * k * X))
+    assert _rel(x, exact.ravel()) < 1e-12
+
+
+def test_cn_advection_conserves_mass_and_l2():
+    """Crank-Nicolson central advection with a discretely divergence-free v is
+    an isometry (Cayley transform of a skew-symmetric operator): ||phi||_2 and
+    sum(phi) are conserved to solver precision, at a Courant number > 1."""
+    nx, ny = 24, 20
+    u, v = _streamfunction_velocity(nx, ny, 2)
+    u, v = u / 50, v / 50
+    rng = np.random.default_rng(5)
+    phi = rng.random((ny, nx))
+    prm = Params(Lambda=0.0, eps=0.0, dt=0.05, startup_be=0)
+    cfl = prm.dt * max(np.abs(u).max() * nx, np.abs(v).max() * ny)
+    assert cfl > 1.0
+    st = State(phi=phi, phi_prev=phi.copy(), c=np.ones((ny, nx)), u=u, v=v, p=np.zeros((ny, nx)))
+    A, b, phs = ch_system(st, prm)
+    x, _ = bicgstab(A, b, phs.ravel(), 1 / A.diagonal(), 1e-13, 5000)
+    assert abs(np.linalg.norm(x) - np.linalg.norm(phi)) < 1e-12 * np.linalg.norm(phi)
+    assert abs(x.sum() - phi.sum()) < 1e-12 * phi.sum()
+    assert _rel(x, phi.ravel()) > 1e-2          # it did move
+
+
+def test_ch_startup_step_is_backward_euler():
+    """With startup_be = 1 the first CH step takes theta = 1 on the Gamma1 term:
+    the eigenmode factor is (1/dt)/(1/dt + G1 L phi0 lam^2) (R23); the second
+    step is Crank-Nicolson again."""
+    nx, ny = 16, 16
+    X, Y = _grid(nx, ny)
+    e = np.cos(2 * np.pi * X) * np.cos(np.pi * 2 * Y)
+    lam = -(4 * nx * nx) * np.sin(np.pi / nx) ** 2 - (4 * ny * ny) * np.sin(np.pi / ny) ** 2
+    phi0, d = 0.3, 1e-3
+    prm = Params(Lambda=0.1, eps=0.0, startup_be=1)
+    z = np.zeros((ny, nx))
+    q = prm.Gamma1 * prm.Lambda * phi0 * lam ** 2
+    for n, g in ((0, (1 / prm.dt) / (1 / prm.dt + q)),
+                 (1, (1 / prm.dt - q / 2) / (1 / prm.dt + q / 2))):
+        st = State(phi=phi0 + d * e, phi_prev=phi0 + 3 * d * e, c=np.ones((ny, nx)), u=z, v=z,
+                   p=z, n=n)
+        A, b, phs = ch_system(st, prm)
+        x, _ = bicgstab(A, b, phs.ravel(), 1.0 / A.diagonal(), 1e-14, 1000)
+        assert _rel(x - phi0, d * g * e.ravel()) < 1e-10
+
+
+# ------------------------------------- momentum pieces against analytic fields
+def _u_points(n):
+    x = np.arange(n)[None, :] / n * np.ones((n, 1))
+    y = (np.arange(n)[:, None] + 0.5) / n * np.ones((1, n))
+    return x, y
+
+
+def _v_points(n):
+    x = (np.arange(n)[None, :] + 0.5) / n * np.ones((n, 1))
+    y = np.arange(n)[:, None] / n * np.ones((1, n))
+    return x, y
+
+
+def _order(errs):
+    return [errs[i] / errs[i + 1] for i in range(len(errs) - 1)]
+
+
+def test_viscous_flux_form_second_order():
+    """div_h(eta grad_h u) on the u points (odd walls) against the analytic
+    div(eta grad s), s = cos(2 pi x) sin(pi y) (zero on the walls), eta =
+    1 + sin(2 pi x) cos(pi y)^2 / 2 (even about the walls): error ratio 4."""
+    errs = []
+    for n in (16, 32, 64):
+        X, Y = _u_points(n)
+        s = np.cos(2 * np.pi * X) * np.sin(np.pi * Y)
+        eta = 1 + 0.5 * np.sin(2 * np.pi * X) * np.cos(np.pi * Y) ** 2
+        sx = -2 * np.pi * np.sin(2 * np.pi * X) * np.sin(np.pi * Y)
+        sy = np.pi * np.cos(2 * np.pi * X) * np.cos(np.pi * Y)
+        ex_ = np.pi * np.cos(2 * np.pi * X) * np.cos(np.pi * Y) ** 2
+        ey_ = -0.5 * np.sin(2 * np.pi * X) * 2 * np.cos(np.pi * Y) * np.sin(np.pi * Y) * np.pi
+        sxx = -4 * np.pi ** 2 * s
+        syy = -np.pi ** 2 * s
+        exact = ex_ * sx + eta * sxx + ey_ * sy + eta * syy
+        got = ex.visc_u_inhom(s, eta, 0.0)
+        errs.append(np.abs(got - exact).max())
+    r = _order(errs)
+    assert all(3.3 < q < 4.7 for q in r), errs
+
+
+def test_viscous_transpose_analytic_and_identity():
+    """R's viscous part div(eta (grad v)^T): (a) shear u = sin(pi y), v = 0 under
+    eta = eta(x): T_x = 0 and T_y = eta'(x) u'(y) at second order; (b) constant eta
+    and a discretely divergence-free v: T = eta grad(div v) = 0 to round-off."""
+    Re_n, Re_s = 0.5, 2.0                       # eta(phi) = phi/Re_n + (1-phi)/Re_s
+    errs = []
+    for n in (16, 32, 64):
+        xc = (np.arange(n) + 0.5) / n
+        phis = np.repeat((0.5 + 0.4 * np.sin(2 * np.pi * xc))[None, :], n, axis=0)
+        Xu, Yu = _u_points(n)
+        u = np.sin(np.pi * Yu)
+        Tx, Ty = ex.visc_transpose(u, np.zeros((n, n)), phis, Re_n, Re_s)
+        assert np.abs(Tx).max() < 1e-9
+        Xv, Yv = _v_points(n)                   # T_y lives on the v points (j >= 1)
+        deta = (1 / Re_n - 1 / Re_s) * 0.4 * 2 * np.pi * np.cos(2 * np.pi * Xv)
+        exact = deta * np.pi * np.cos(np.pi * Yv)
+        errs.append(np.abs(Ty[1:] - exact[1:]).max())
+    assert all(3.3 < q < 4.7 for q in _order(errs)), errs
+    nx, ny = 12, 10
+    us, vs = _streamfunction_velocity(nx, ny, 3)
+    Tx, Ty = ex.visc_transpose(us, vs, np.full((ny, nx), 0.3), Re_n, Re_s)
+    assert np.abs(Tx).max() < 1e-9 * np.abs(us).max() * nx * nx
+    assert np.abs(Ty).max() < 1e-9 * np.abs(us).max() * nx * nx
+
+
+def test_convective_terms_second_order():
+    """(v·∇)u on the u points and (v·∇)v on the v points against analytic
+    fields: u = U + sin(2 pi x) sin(pi y) ... evaluated where each lives."""
+    eu, ev = [], []
+    for n in (16, 32, 64):
+        Xu, Yu = _u_points(n)
+        Xv, Yv = _v_points(n)
+        A, B = 0.7, 0.4
+        # u = A sin(2 pi x) sin(pi y) (zero on the walls, lid 0);  v = B sin(2 pi x) sin(pi y)
+        uf = lambda x, y: A * np.sin(2 * np.pi * x) * np.sin(np.pi * y)
+        vf = lambda x, y: B * np.sin(2 * np.pi * x) * np.sin(np.pi * y)
+        u, v = uf(Xu, Yu), vf(Xv, Yv)
+        v[0] = 0.0
+        ux = lambda x, y: A * 2 * np.pi * np.cos(2 * np.pi * x) * np.sin(np.pi * y)
+        uy = lambda x, y: A * np.pi * np.sin(2 * np.pi * x) * np.cos(np.pi * y)
+        vx = lambda x, y: B * 2 * np.pi * np.cos(2 * np.pi * x) * np.sin(np.pi * y)
+        vy = lambda x, y: B * np.pi * np.sin(2 * np.pi * x) * np.cos(np.pi * y)
+        cu = uf(Xu, Yu) * ux(Xu, Yu) + vf(Xu, Yu) * uy(Xu, Yu)
+        cv = uf(Xv, Yv) * vx(Xv, Yv) + vf(Xv, Yv) * vy(Xv, Yv)
+        eu.append(np.abs(ex.convective_u(u, v, 0.0) - cu).max())
+        ev.append(np.abs((ex.convective_v(u, v) - cv)[1:]).max())
+    assert all(3.3 < q < 4.7 for q in _order(eu)), eu
+    assert all(3.3 < q < 4.7 for q in _order(ev)), ev
+
+
+def test_phase_stress_second_order():
+    """R = -G1 div(grad phi (x) grad phi) for phi = cos(2 pi x) cos(pi y) against
+    the analytic divergence (all of T_xx, T_yy, T_xy enter), error ratio 4."""
+    G1 = 1.3
+    ex_, ey_ = [], []
+    for n in (16, 32, 64):
+        X, Y = _grid(n, n)
+        phi = np.cos(2 * np.pi * X) * np.cos(np.pi * Y)
+        p = lambda x, y: np.cos(2 * np.pi * x) * np.cos(np.pi * y)
+        px = lambda x, y: -2 * np.pi * np.sin(2 * np.pi * x) * np.cos(np.pi * y)
+        py = lambda x, y: -np.pi * np.cos(2 * np.pi * x) * np.sin(np.pi * y)
+        pxx = lambda x, y: -4 * np.pi ** 2 * p(x, y)
+        pyy = lambda x, y: -np.pi ** 2 * p(x, y)
+        pxy = lambda x, y: 2 * np.pi ** 2 * np.sin(2 * np.pi * x) * np.sin(np.pi * y)
+        # div(grad phi grad phi) = (lap phi) grad phi + grad(|grad phi|^2)/2
+        rx = lambda x, y: -G1 * ((pxx(x, y) + pyy(x, y)) * px(x, y)
+                                 + px(x, y) * pxx(x, y) + py(x, y) * pxy(x, y))
+        ry = lambda x, y: -G1 * ((pxx(x, y) + pyy(x, y)) * py(x, y)
+                                 + px(x, y) * pxy(x, y) + py(x, y) * pyy(x, y))
+        Rx, Ry = ex.phase_stress(phi, G1)
+        Xu, Yu = _u_points(n)
+        Xv, Yv = _v_points(n)
+        ex_.append(np.abs(Rx - rx(Xu, Yu)).max())
+        ey_.append(np.abs((Ry - ry(Xv, Yv))[1:]).max())
+    assert all(3.3 < q < 4.7 for q in _order(ex_)), ex_
+    assert all(3.3 < q < 4.7 for q in _order(ey_)), ey_
+
+
+def test_growth_uniform_state_closed_form():
+    """Uniform phi0, c0, v = 0: one CH step adds exactly dt eps mu phi0 c0/(K_c + c0)
+    (Eq. 5 by hand) -- and nothing for phi0 < 0 (volume fraction, R24)."""
+    n = 8
+    z = np.zeros((n, n))
+    prm = Params(dt=0.01, eps=1.0, mu=0.14, Kc=0.15, lid_u=0.0, rtol=1e-14)
+    for phi0, c0, gain in ((0.3, 0.8, 0.01 * 0.14 * 0.3 * 0.8 / 0.95), (-0.01, 0.8, 0.0)):
+        st = State(phi=np.full((n, n), phi0), phi_prev=np.full((n, n), phi0),
+                   c=np.full((n, n), c0), u=z, v=z, p=z)
+        A, b, phs = ch_system(st, prm)
+        x, _ = bicgstab(A, b, phs.ravel(), 1 / A.diagonal(), 1e-14, 100)
+        assert np.abs(x - (phi0 + gain)).max() < 1e-15 + 1e-13 * abs(phi0)
+
+
+@pytest.mark.parametrize("phi0", [0.3, 0.7, 0.05])
+def test_fprime_linear_growth_rate(phi0):
+    """Gamma1 = 0, v = 0, no production, phi^n = phi^{n-1} = phi0 + d e (e a
+    Laplacian eigenmode with eigenvalue lam): one CH step multiplies the mode by
+    1 + dt Lambda phi0 F''(phi0) lam + O(d), with F''(phi) = 2 Gamma2 (1 - 6 phi
+    + 6 phi^2) the second derivative of Gamma2 phi^2 (1 - phi)^2 (Eq. 16 energy,
+    PAPER.md:113).  Two amplitudes extrapolate the O(d) term away."""
+    nx, ny = 16, 12
+    X, Y = _grid(nx, ny)
+    e = np.cos(2 * np.pi * X) * np.cos(np.pi * Y)
+    lam = -(4 * nx * nx) * np.sin(np.pi / nx) ** 2 - (4 * ny * ny) * np.sin(np.pi / (2 * ny)) ** 2
+    prm = Params(Gamma1=0.0, Gamma2=2.0, Lambda=1.0, eps=0.0, dt=0.01, lid_u=0.0)
+    z = np.zeros((ny, nx))
+    amps = []
+    for d in (1e-4, 2e-4):
+        phi = phi0 + d * e
+        st = State(phi=phi, phi_prev=phi.copy(), c=np.ones((ny, nx)), u=z, v=z, p=z)
+        A, b, phs = ch_system(st, prm)
+        x = b * prm.dt                                   # A = I/dt exactly (Gamma1 = 0, v = 0)
+        amps.append(float(np.dot(x - phi0, e.ravel()) / np.dot(e.ravel(), e.ravel())) / d)
+    g = 2 * amps[0] - amps[1]                            # Richardson in d
+    F2 = 2 * prm.Gamma2 * (1 - 6 * phi0 + 6 * phi0 ** 2)
+    expect = 1 + prm.dt * prm.Lambda * phi0 * F2 * lam
+    assert abs(expect - 1) > 1e-3                        # the pin is non-trivial
+    assert abs(g - expect) < 1e-6 * abs(expect - 1)
