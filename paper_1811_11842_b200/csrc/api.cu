@@ -82,7 +82,8 @@ struct ch_handle {
   int cg_defer = 64;          // block length m (2..64) of the deferred p/x CG (env CHB_DEFER);
                               // reduced at ch_create if the z history would not fit
   double* gm_dev = nullptr;   // GMRES dot results / coefficients (device, 192)
-  double* gm_host = nullptr;  // pinned mirror
+  double* gm_host = nullptr;  // pinned mirror (max(192, 72 * slabs) doubles)
+  double* gm_red = nullptr;   // GMRES per-slab dot results, device [slabs + 1][72]
   int cg3 = 1;                // single-reduction CG: three-term z recurrence (env CHB_CG3)
   int strip2 = 0;             // rows per strip, 0 = one resident wave (env CHB_STRIP)
   int pdl = 1;                // programmatic dependent launch of the CG sweeps (env CHB_PDL)
@@ -383,6 +384,7 @@ OpDesc opdesc(ch_handle* h, int kind, const Slab& s) {
   d.w = nullptr;
   d.s = 1.0;
   d.kscale = 1.0;
+  d.ascal = 0.0;
   d.rho_n = h->prm.rho_n;
   d.rho_s = h->prm.rho_s;
   switch (kind) {
@@ -390,7 +392,15 @@ OpDesc opdesc(ch_handle* h, int kind, const Slab& s) {
     case OPK_POISSON_VAR: d.w = s.a[A_PHI1]; break;
     case OPK_NUTRIENT: d.a = s.a[A_CA]; d.w = s.a[A_CW]; d.s = 0.5; d.kscale = h->prm.Ds; break;
     case OPK_MOM_U:
-    case OPK_MOM_V: d.a = s.a[A_CA]; d.w = s.a[A_CW]; d.s = h->prm.theta_visc; break;
+    case OPK_MOM_V:
+      d.a = s.a[A_CA];
+      d.w = s.a[A_CW];
+      d.s = h->prm.theta_visc;
+      if (h->prm.rho_n == h->prm.rho_s) {  // a = rho/dt is one number: no a[] stream
+        d.kind = kind == OPK_MOM_U ? OPK_MOM_U_C : OPK_MOM_V_C;
+        d.ascal = h->prm.rho_s / h->prm.dt;
+      }
+      break;
   }
   return d;
 }
@@ -416,6 +426,7 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   for (int k = 2; k < NZ; ++k) Zr[k] = A_ZH0 + (k - 2);
   const int S[2] = {A_RH, A_BP}, P = A_PA;
   const double cells = (double)h->grid.nx * (double)h->nrows / h->S;
+  const int ekind = opdesc(h, kind, h->sl[0]).kind;  // kind the kernels run (bytes per cell)
   const double* tab = h->cgtab + (size_t)sys * 2 * CGT;
   auto px = [&](long k_last, int n, int write_p) -> int {
     // z_k of iterations k_last - n + 1 .. k_last
@@ -492,7 +503,7 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
     // algorithmic bytes of the launch: K sweeps + the in-kernel p/x updates
     const long K = h->sch[sys].iter;
     if (!h->tm.pending.empty() && h->tm.pending.back().kc == kc_sys)
-      h->tm.pending.back().bytes = (cgs_bytes(kind, 0, 1) * (double)K +
+      h->tm.pending.back().bytes = (cgs_bytes(ekind, 0, 1) * (double)K +
                                     8.0 * (m + 4) * (double)(K / m)) * cells;
   } else {
   const int tt = h->cg3 && NZ >= 3;
@@ -506,7 +517,7 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
       // and writes no s
       const int si = tt ? Zr[(k + NZ - 1) % NZ] : S[(k + 1) & 1], so = tt ? -1 : S[k & 1];
       {
-        KTime kt(h, kc_sys, cgs_bytes(kind, first, tt) * cells, k + 1);
+        KTime kt(h, kc_sys, cgs_bytes(ekind, first, tt) * cells, k + 1);
         for (int s = 0; s < h->S; ++s) {
           Slab& sl = h->sl[s];
           launch_cgs_iter(opdesc(h, kind, sl), sl.g, sl.a[zi], sl.a[zo], sl.a[si],
@@ -821,19 +832,35 @@ int zero_vrow0(ch_handle* h) {
 namespace {
 
 int gm_dots(ch_handle* h, int k, int wvec, std::vector<double>& out) {
-  // out[i] = (V_i, V_wvec) for i < k, summed over slabs in slab order (and ranks)
+  // out[i] = (V_i, V_wvec) for i < k, summed over slabs in slab order, then over
+  // ranks by one in-place device allreduce of all k values (one host round trip)
   out.assign(k, 0.0);
-  for (auto& s : h->sl) {
-    launch_gm_dots(s.g, s.V.data(), k, s.V[wvec], h->gm_dev, h->part, h->ticket, h->st);
-    CK(cudaMemcpyAsync(h->gm_host, h->gm_dev, k * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    for (int i = 0; i < k; ++i) out[i] += h->gm_host[i];
+  for (int s = 0; s < h->S; ++s) {
+    Slab& sl = h->sl[s];
+    launch_gm_dots(sl.g, sl.V.data(), k, sl.V[wvec], h->gm_red + (size_t)s * 72, h->part,
+                   h->ticket, h->st);
   }
   h->stats.launches += h->S;
   h->stats.kc_launches[CH_KC_GMRES] += h->S;
-  if (h->comm)
-    for (int i = 0; i < k; ++i) out[i] = comm_allreduce_host(h->comm, out[i]);
-  return check_launch(h, "gm_dots");
+  TRY(check_launch(h, "gm_dots"));
+  CK(cudaMemcpyAsync(h->gm_host, h->gm_red, (size_t)h->S * 72 * sizeof(double),
+                     cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  for (int s = 0; s < h->S; ++s)
+    for (int i = 0; i < k; ++i) out[i] += h->gm_host[(size_t)s * 72 + i];
+  if (h->comm) {
+    for (int i = 0; i < k; ++i) h->gm_host[i] = out[i];
+    CK(cudaMemcpyAsync(h->gm_red, h->gm_host, k * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    double* sum = h->gm_red + (size_t)h->S * 72;  // distinct receive buffer
+    if (comm_allreduce_sum(h->comm, h->gm_red, sum, (size_t)k, h->st) != 0) {
+      h->err = "gmres: allreduce of the Gram-Schmidt dots failed";
+      return CH_ERR_COMM;
+    }
+    CK(cudaMemcpyAsync(h->gm_host, sum, k * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    for (int i = 0; i < k; ++i) out[i] = h->gm_host[i];
+  }
+  return CH_OK;
 }
 
 int gm_set_coef(ch_handle* h, const double* v, int k) {
@@ -1019,6 +1046,7 @@ static void destroy_mem(ch_handle* h) {
   if (h->tot) cudaFree(h->tot);
   if (h->tot_local) cudaFree(h->tot_local);
   if (h->gm_dev) cudaFree(h->gm_dev);
+  if (h->gm_red) cudaFree(h->gm_red);
   if (h->cgtab) cudaFree(h->cgtab);
   if (h->pbar) cudaFree(h->pbar);
   if (h->gm_host) cudaFreeHost(h->gm_host);
@@ -1129,7 +1157,8 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
       cudaMalloc(&h->gm_dev, 192 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&h->cgtab, (size_t)NSC * 2 * CGT * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&h->pbar, 4 * sizeof(unsigned int)) != cudaSuccess ||
-      cudaMallocHost(&h->gm_host, 192 * sizeof(double)) != cudaSuccess)
+      cudaMalloc(&h->gm_red, (size_t)(S + 1) * 72 * sizeof(double)) != cudaSuccess ||
+      cudaMallocHost(&h->gm_host, (size_t)std::max(192, 72 * S) * sizeof(double)) != cudaSuccess)
     return fail(CH_ERR_CUDA, h, "cudaMalloc (scalars)");
   cudaMemset(h->sc, 0, NSC * sizeof(KScal));
   memset(h->sch, 0, NSC * sizeof(KScal));

@@ -57,7 +57,6 @@ NcclApi& api() {
 struct Comm {
   ncclComm_t comm;
   int rank, nranks;
-  double* scratch;  // device, 2 doubles (host allreduce)
 };
 
 int comm_unique_id(void* out, size_t len) {
@@ -92,7 +91,6 @@ Comm* comm_create(const void* id, size_t len, int rank, int nranks, int device, 
     delete c;
     return nullptr;
   }
-  cudaMalloc(&c->scratch, 2 * sizeof(double));
   return c;
 }
 
@@ -146,17 +144,13 @@ int comm_iter_exchange(Comm* c, const double* send, double* recv, size_t count,
   return bad ? 1 : 0;
 }
 
-double comm_allreduce_host(Comm* c, double v) {
-  cudaMemcpy(c->scratch, &v, sizeof v, cudaMemcpyHostToDevice);
-  api().AllReduce(c->scratch, c->scratch + 1, 1, ncclFloat64, ncclSum, c->comm, 0);
-  double out = 0.0;
-  cudaMemcpy(&out, c->scratch + 1, sizeof out, cudaMemcpyDeviceToHost);
-  return out;
+int comm_allreduce_sum(Comm* c, const double* send, double* recv, size_t count, cudaStream_t st) {
+  return api().AllReduce(send, recv, count, ncclFloat64, ncclSum, c->comm, st) == ncclSuccess ? 0
+                                                                                              : 1;
 }
 
 void comm_destroy(Comm* c) {
   if (!c) return;
   api().CommDestroy(c->comm);
-  cudaFree(c->scratch);
   delete c;
 }

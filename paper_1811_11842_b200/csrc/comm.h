@@ -29,5 +29,6 @@ struct HaloSpec {
 };
 int comm_iter_exchange(Comm* c, const double* send, double* recv, size_t count,
                        const HaloSpec* halos, int nhalo, int pitch, cudaStream_t st);
-double comm_allreduce_host(Comm* c, double v);
+// recv = sum over ranks of send (`count` device doubles, distinct buffers), on stream st (0 = ok)
+int comm_allreduce_sum(Comm* c, const double* send, double* recv, size_t count, cudaStream_t st);
 void comm_destroy(Comm* c);

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(128) k_cg5_init(Geom g, Op5T op, const double*
       if (col.needW) ww = ldf<BC_MIRROR>(op.w, g, gj, col.cw);
       if (col.needE) we = ldf<BC_MIRROR>(op.w, g, gj, col.ce);
     }
-    const double ac = AM ? op.a[off(g, gj, col.cc)] : 0.0;
+    const double ac = a_at<AM>(op, off(g, gj, col.cc));
     double y, d;
     eval5T<BC, AM, KM>(op, g, gj, ac, w0, ww, we, wm, wp, x0, xw, xe, xm, xp, y, d);
     if (col.act) {
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(128) k_op5_apply(Geom g, Op5T op, const double
       if (col.needW) ww = ldf<BC_MIRROR>(op.w, g, gj, col.cw);
       if (col.needE) we = ldf<BC_MIRROR>(op.w, g, gj, col.ce);
     }
-    const double ac = AM ? op.a[off(g, gj, col.cc)] : 0.0;
+    const double ac = a_at<AM>(op, off(g, gj, col.cc));
     double y, d;
     eval5T<BC, AM, KM>(op, g, gj, ac, w0, ww, we, wm, wp, x0, xw, xe, xm, xp, y, d);
     if (col.act) yout[off(g, gj, col.c)] = y;
@@ -199,6 +199,7 @@ static Op5T make_op(const OpDesc& d) {
   o.kscale = d.kscale;
   o.rho_n = d.rho_n;
   o.rho_s = d.rho_s;
+  o.ascal = d.ascal;
   return o;
 }
 
@@ -213,6 +214,8 @@ static dim3 grid5(const Geom& g, int strip) {
     case OPK_NUTRIENT:      { constexpr int BC = BC_MIRROR, AM = 1, KM = 1; CALL; } break; \
     case OPK_MOM_U:         { constexpr int BC = BC_ODD,    AM = 1, KM = 1; CALL; } break; \
     case OPK_MOM_V:         { constexpr int BC = BC_VFACE,  AM = 1, KM = 1; CALL; } break; \
+    case OPK_MOM_U_C:       { constexpr int BC = BC_ODD,    AM = 2, KM = 1; CALL; } break; \
+    case OPK_MOM_V_C:       { constexpr int BC = BC_VFACE,  AM = 2, KM = 1; CALL; } break; \
     default: break;                                                     \
   }
 

@@ -11,7 +11,9 @@ enum OpKind : int {
   OPK_POISSON_VAR = 1,
   OPK_NUTRIENT = 2,
   OPK_MOM_U = 3,
-  OPK_MOM_V = 4
+  OPK_MOM_V = 4,
+  OPK_MOM_U_C = 5,   // momentum with constant density: a = rho/dt is a scalar (rho_n == rho_s)
+  OPK_MOM_V_C = 6
 };
 
 // Operator descriptor for the 5-point family (op5.cuh, kernels_aux.cu, kernels_cgs.cu).
@@ -23,6 +25,7 @@ struct OpDesc {
   const double* a;    // diagonal coefficient array (NUTRIENT, MOM_*)
   const double* w;    // cell coefficient (NUTRIENT: phi_s^{1/2}; POISSON_VAR: phi^{n+1})
   double s, kscale, rho_n, rho_s;
+  double ascal;       // the diagonal coefficient of the *_C kinds
 };
 
 void launch_cg5_init(const OpDesc& d, const Geom& g, const double* x, const double* b,

@@ -11,7 +11,14 @@ struct Op5T {
   const double* a;
   const double* w;
   double s, kscale, rho_n, rho_s;
+  double ascal;   // AM == 2: constant diagonal coefficient (no array)
 };
+
+// diagonal coefficient at flat offset o: AM = 0 none, 1 array a[], 2 scalar
+template <int AM>
+__device__ __forceinline__ double a_at(const Op5T& op, size_t o) {
+  return AM == 2 ? op.ascal : (AM ? op.a[o] : 0.0);
+}
 
 template <int KM>
 __device__ __forceinline__ double kfaceT(const Op5T& op, double w1, double w2) {
