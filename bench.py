@@ -255,6 +255,18 @@ def run_ours(args, rank, world, local_rank):
                             "how": "extrapolated, not measured: measured 256^2 step x cells "
                                    "ratio x Krylov-iteration ratio"}}
 
+    # BASELINE configs[4]'s isolated matvec sweeps (rank 0, after the timed region)
+    mv = None
+    if rank == 0 and world == 1 and args.matvec:
+        try:
+            from paper_1811_11842_b200.matvec import sweep
+            sim.close()
+            torch.cuda.empty_cache()
+            mv = {"records": sweep(tuple(args.matvec_sizes), 20, peak), "peak_gbs": peak,
+                  "workload": "configs[4] isolated CH / Poisson applies, random [0,1) fields"}
+        except Exception as e:   # never lose the headline line to the side measurement
+            mv = {"error": repr(e)[:300]}
+
     if rank == 0:
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         line = {"metric": METRIC, "value": value, "unit": "time-steps/s", "n_gpus": world,
@@ -270,7 +282,8 @@ def run_ours(args, rank, world, local_rank):
                            "krylov_iters_per_step": iters_step},
                 "cell_steps_per_s": value * nx * ny,
                 "roofline": roof, "kernels": per_class, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": st["launches"] * world, "clocks": clk.summary()}
+                "gpu_launches": st["launches"] * world, "clocks": clk.summary(),
+                "matvec_sweep": mv}
         print(json.dumps(line), flush=True)
     sim.close()
     if world > 1:
@@ -295,6 +308,8 @@ def parse_args(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--matvec", type=int, default=1, help="1: add configs[4]'s matvec sweep")
+    ap.add_argument("--matvec-sizes", type=int, nargs="+", default=[1024, 4096, 16384])
     args = ap.parse_args(argv)
     if args.steps is None:
         args.steps = CONFIGS[args.config]["steps"]

@@ -1313,7 +1313,9 @@ int ch_apply_operator(ch_handle* h, int op, const double* x, double* y, int wher
   const double cells = (double)h->grid.nx * (double)h->nrows / h->S;
   if (kind < 0) {
     TRY(halo(h, A_TMP, 2));
-    KTime kt(h, CH_KC_CH_APPLY, 24.0 * cells);   // read x, phi*; write y
+    // read x, phi* (+ u, v of the advection part); write y
+    const bool adv = phys_at(h->prm, h->tidx).th_adv != 0.0;
+    KTime kt(h, CH_KC_CH_APPLY, (adv ? 40.0 : 24.0) * cells);
     for (int s = 0; s < h->S; ++s) {
       Slab& sl = h->sl[s];
       launch_ch_apply(sl.g, chcoef(h, sl, false), sl.a[A_TMP], sl.a[A_B], 0, nullptr, nullptr, 0,

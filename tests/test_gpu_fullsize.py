@@ -80,6 +80,7 @@ def test_full_size_operator_samples_match_oracle():
     x = rng.random((n, n))
     rho_n, rho_s = 1.4, 0.8
     sim = Simulation(n, n, rho_n=rho_n, rho_s=rho_s, Lambda=1e-5)
+    sim.time_index = 10          # past the backward-Euler start-up: the CN weights apply
     sp = sim.params
     sim.set_fields(**f)
     yp = sim.apply_operator("poisson", x)

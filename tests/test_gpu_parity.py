@@ -178,6 +178,7 @@ def test_operator_applies_match_assembled_matrices():
     sim = Simulation(nx, ny, Lambda=1e-3)
     prm = oracle_params(sim.params)
     sim.set_fields(**f)
+    sim.time_index = 10      # past the backward-Euler start-up: CN weights (R23)
     st = initial_state(f)
     phs = ex.phi_star(st.phi, st.phi_prev)
     Mx, My = ex.mobility_faces(phs, prm.Lambda)
@@ -334,6 +335,7 @@ def _solve_case(nx, ny, op, seed=0, **over):
     prm = oracle_params(sp)
     sim = Simulation(nx, ny, sp)
     sim.set_fields(**f)
+    sim.time_index = 10      # past the backward-Euler start-up: CN weights (R23)
     x = sim.solve(op, b, x0)
     st = sim.stats()
     sim.close()
@@ -359,40 +361,49 @@ def _solve_case(nx, ny, op, seed=0, **over):
     return x, ref.reshape(ny, nx), st["iters_last"][sysname], it
 
 
-def _true_rel_residual(op, nx, ny, x, b_seed=0, **over):
-    """||b - A x|| / ||b|| with the oracle's assembled matrix (same state, same b)."""
+def _momentum_matrix(op, nx, ny, seed=0, **over):
     from paper_1811_11842_b200 import SimParams
-    from oracle import assemble as asm, explicit as ex
+    from oracle import explicit as ex
     from oracle.step import initial_state, momentum_systems
     from workloads import initial_fields
-    f = initial_fields(nx, ny, seed=b_seed)
-    f["u"], f["v"] = stream_velocity(nx, ny, seed=b_seed + 1, scale=0.02)
-    b = np.random.default_rng(b_seed + 11).standard_normal((ny, nx))
+    f = initial_fields(nx, ny, seed=seed)
     s0 = initial_state(f)
-    prm = oracle_params(SimParams(**over))
-    phs = ex.phi_star(s0.phi, s0.phi_prev)
-    (Au, _), (Av, _) = momentum_systems(s0, phs, prm)
-    A = Au if op == "mom_u" else Av
+    (Au, _), (Av, _) = momentum_systems(s0, ex.phi_star(s0.phi, s0.phi_prev),
+                                        oracle_params(SimParams(**over)))
+    return Au if op == "mom_u" else Av
+
+
+def _check_momentum_solve(op, nx, ny, x, ref, it_gpu, it_ref, seed=0, **over):
+    """The momentum operators carry the viscosity contrast eta(0.3)/eta(0) ~ 1e5
+    (R6): for a random b, neither fp64 CG attains a TRUE residual near rtol
+    (attainable accuracy ~ eps kappa).  The GPU solve must match the textbook
+    CG's own true residual (same iterates in exact arithmetic, rounding order
+    differs) and its iteration count."""
+    A = _momentum_matrix(op, nx, ny, seed, **over)
+    b = np.random.default_rng(seed + 11).standard_normal((ny, nx))
     if op == "mom_v":
         b[0] = 0.0
-    return float(np.linalg.norm(b.ravel() - A @ x.ravel()) / np.linalg.norm(b))
+    bn = np.linalg.norm(b)
+    t_gpu = np.linalg.norm(b.ravel() - A @ x.ravel()) / bn
+    t_ref = np.linalg.norm(b.ravel() - A @ ref.ravel()) / bn
+    assert t_gpu <= max(2e-12, 10.0 * t_ref), (op, t_gpu, t_ref)
+    assert rel(x, ref) <= 1e-5, (op, rel(x, ref))
+    # rtol 1e-12 sits near this system's attainable accuracy: the last iterations are
+    # rounding-order dependent
+    assert abs(it_gpu - it_ref) <= 2 + 0.05 * it_ref, (it_gpu, it_ref)
 
 
 @pytest.mark.parametrize("op", ["poisson", "mom_u", "mom_v", "ch"])
 @pytest.mark.parametrize("nx,ny", [(64, 48), (300, 37)])
 def test_isolated_solve_matches_oracle(op, nx, ny):
-    """Same b, x0 and coefficients on both sides.  The momentum operators carry
-    the viscosity contrast eta(0.3)/eta(0) ~ 1e5 (R6), so for a random b the
-    solution itself is determined only to ~kappa * rtol: there the check is
-    the TRUE residual under the oracle's assembled matrix plus the iteration
-    count (the same CG iterates in exact arithmetic), elsewhere the fields."""
+    """Same b, x0 and coefficients on both sides (see _check_momentum_solve for
+    the momentum operators)."""
     over = dict(rtol=1e-12, Lambda=1e-5, rho_n=1.3)
     x, ref, it_gpu, it_ref = _solve_case(nx, ny, op, **over)
     if op in ("mom_u", "mom_v"):
-        assert _true_rel_residual(op, nx, ny, x, **over) <= 2e-12
-        assert rel(x, ref) <= 1e-5, (op, rel(x, ref))
-    else:
-        assert rel(x, ref) <= 1e-9, (op, rel(x, ref))
+        _check_momentum_solve(op, nx, ny, x, ref, it_gpu, it_ref, **over)
+        return
+    assert rel(x, ref) <= 1e-9, (op, rel(x, ref))
     if op == "ch":
         # BiCGStab's count is not a function of the arithmetic alone (the
         # oracle itself moves by tens of iterations when b is perturbed by 1e-15)
@@ -407,10 +418,10 @@ def test_isolated_solve_deferred_modes(defer, op, monkeypatch):
     monkeypatch.setenv("CHB_DEFER", defer)
     x, ref, it_gpu, it_ref = _solve_case(128, 96, op, rtol=1e-12, rho_n=0.7)
     if op == "mom_v":
-        assert _true_rel_residual(op, 128, 96, x, rtol=1e-12, rho_n=0.7) <= 2e-12
+        _check_momentum_solve(op, 128, 96, x, ref, it_gpu, it_ref, rtol=1e-12, rho_n=0.7)
     else:
         assert rel(x, ref) <= 1e-9, (op, rel(x, ref))
-    assert abs(it_gpu - it_ref) <= 2, (it_gpu, it_ref)
+        assert abs(it_gpu - it_ref) <= 2, (it_gpu, it_ref)
 
 
 @pytest.mark.parametrize("op", ["poisson", "mom_v"])
@@ -419,7 +430,7 @@ def test_persistent_isolated_solve(op, monkeypatch):
     monkeypatch.setenv("CHB_DEFER", "5")
     x, ref, it_gpu, it_ref = _solve_case(128, 96, op, rtol=1e-12, rho_n=0.7)
     if op == "mom_v":
-        assert _true_rel_residual(op, 128, 96, x, rtol=1e-12, rho_n=0.7) <= 2e-12
+        _check_momentum_solve(op, 128, 96, x, ref, it_gpu, it_ref, rtol=1e-12, rho_n=0.7)
     else:
         assert rel(x, ref) <= 1e-9, (op, rel(x, ref))
-    assert abs(it_gpu - it_ref) <= 2, (it_gpu, it_ref)
+        assert abs(it_gpu - it_ref) <= 2, (it_gpu, it_ref)
