@@ -73,7 +73,9 @@ enum {
   CH_OP_CH = 0,       /* y = [I/dt + th G1 L_{M*} Delta_h + ta Adv(.; v^n)] x, M* from phi, phi_prev */
   CH_OP_POISSON = 1,  /* y = -D_h beta G_h x, beta = 1/rho(current phi) on faces (Eq. 20 LHS)      */
   CH_OP_MOM_U = 2,    /* y = [a - theta_visc Delta_h^0] x on x-faces, a = 1/(nu(phi*) dt)          */
-  CH_OP_MOM_V = 3     /* same on y-faces, wall row identity                                       */
+  CH_OP_MOM_V = 3,    /* same on y-faces, wall row identity                                       */
+  CH_OP_NUTRIENT = 4  /* y = [diag(f_s/dt + A/2 f) - 1/2 div(K grad)] x, the nutrient system of   */
+                      /* Eq. 16 (3rd line) with phi^{n+1} = phi^{n} = the current phi (R11, R24)  */
 };
 
 /* Krylov method for the (nonsymmetric) Cahn-Hilliard system. */
@@ -231,7 +233,7 @@ int ch_apply_operator(ch_handle* h, int op, const double* x, double* y, int wher
  * Listing 5).  x: initial guess in, solution out (nrows x nx, same `where`
  * as b).  Stops at ||r||_2 <= rtol ||b||_2 (R13); the iteration count and
  * final residual land in ch_stats.{iters_last,resid_last}[system]
- * (CH_SYS_CH, CH_SYS_P, CH_SYS_U, CH_SYS_V).  Returns CH_ERR_NOT_CONVERGED /
+ * (CH_SYS_CH, CH_SYS_P, CH_SYS_U, CH_SYS_V, CH_SYS_NUTRIENT).  Returns CH_ERR_NOT_CONVERGED /
  * CH_ERR_BREAKDOWN like ch_step.  Does not advance the state. */
 int ch_solve(ch_handle* h, int op, const double* b, double* x, int where);
 

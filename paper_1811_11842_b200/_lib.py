@@ -17,7 +17,7 @@ CH_OK, CH_ERR_ARG, CH_ERR_CUDA, CH_ERR_NOT_CONVERGED, CH_ERR_BREAKDOWN, CH_ERR_C
 CH_HOST, CH_DEVICE = 0, 1
 FIELDS = {"phi": 0, "phi_prev": 1, "c": 2, "u": 3, "v": 4, "p": 5}
 SYSTEMS = ("ch", "nutrient", "u", "v", "p")
-OPS = {"ch": 0, "poisson": 1, "mom_u": 2, "mom_v": 3}
+OPS = {"ch": 0, "poisson": 1, "mom_u": 2, "mom_v": 3, "nutrient": 4}
 SOLVERS = {"bicgstab": 0, "gmres": 1}
 KERNEL_CLASSES = ("cg_A", "cg_B", "cg_init", "ch_apply", "vec", "rhs", "gmres", "cg_fused_c",
                   "cg_fused_u", "cg_fused_v", "cg_fused_p", "cg_px", "op_apply")

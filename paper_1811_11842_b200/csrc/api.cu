@@ -1297,6 +1297,14 @@ int prep_operator(ch_handle* h, int op, int* kind) {
       }
       *kind = (op == CH_OP_MOM_U) ? OPK_MOM_U : OPK_MOM_V;
       break;
+    case CH_OP_NUTRIENT:
+      // the nutrient system of a step whose CH solve returned phi^{n+1} = phi^n
+      TRY(copy_arr(h, A_PHI, A_PHI1));
+      TRY(halo(h, A_PHI1, 1));
+      for (auto& s : h->sl)
+        launch_nut_rhs(s.g, ph, state(s), s.a[A_PHI1], s.a[A_CA], s.a[A_CW], s.a[A_TMP2], h->st);
+      *kind = OPK_NUTRIENT;
+      break;
     default:
       h->err = "bad operator id";
       return CH_ERR_ARG;
@@ -1323,9 +1331,12 @@ int ch_apply_operator(ch_handle* h, int op, const double* x, double* y, int wher
     }
   } else {
     TRY(halo(h, A_TMP, 1));
-    if (kind == OPK_MOM_U || kind == OPK_MOM_V) TRY(halo(h, A_CW, 1));
-    // x, y (+ w) (+ a)
-    const double bpc = kind == OPK_POISSON_CONST ? 16.0 : (kind == OPK_POISSON_VAR ? 24.0 : 32.0);
+    if (kind == OPK_MOM_U || kind == OPK_MOM_V || kind == OPK_NUTRIENT) TRY(halo(h, A_CW, 1));
+    // x, y (+ w) (+ a[])
+    const int ek = opdesc(h, kind, h->sl[0]).kind;
+    const double bpc = ek == OPK_POISSON_CONST ? 16.0
+                     : (ek == OPK_POISSON_VAR || ek == OPK_MOM_U_C || ek == OPK_MOM_V_C) ? 24.0
+                     : 32.0;
     KTime kt(h, CH_KC_OP_APPLY, bpc * cells);
     for (auto& s : h->sl) launch_op5_apply(opdesc(h, kind, s), s.g, s.a[A_TMP], s.a[A_B], h->st);
   }
@@ -1346,7 +1357,9 @@ int ch_solve(ch_handle* h, int op, const double* b, double* x, int where) {
   if (kind < 0) {
     TRY(bicgstab_or_gmres(h, A_US, A_B));
   } else {
-    sys = (op == CH_OP_POISSON) ? CH_SYS_P : (op == CH_OP_MOM_U ? CH_SYS_U : CH_SYS_V);
+    sys = (op == CH_OP_POISSON) ? CH_SYS_P
+        : (op == CH_OP_MOM_U) ? CH_SYS_U
+        : (op == CH_OP_MOM_V) ? CH_SYS_V : CH_SYS_NUTRIENT;
     const int ns = (op == CH_OP_POISSON);
     if (ns) {
       for (int s = 0; s < h->S; ++s) {

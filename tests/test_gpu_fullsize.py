@@ -37,12 +37,12 @@ def _true_residual_4096(op, kind, refine=0):
         r -= r.mean()
     st = sim.stats()
     sim.close()
-    sysname = {"poisson": "p", "mom_u": "u", "mom_v": "v"}[op]
+    sysname = {"poisson": "p", "mom_u": "u", "mom_v": "v", "nutrient": "nutrient"}[op]
     return float(torch.linalg.norm(r) / torch.linalg.norm(b)), st["resid_last"][sysname], \
         st["iters_last"][sysname]
 
 
-@pytest.mark.parametrize("op", ["poisson", "mom_u"])
+@pytest.mark.parametrize("op", ["poisson", "mom_u", "nutrient"])
 def test_full_size_solve_true_residual(op):
     """4096^2: the recursively updated residual the solver stops on is the true
     one, ||b - A x|| <= 2 rtol ||b||, with A applied by the independent apply

@@ -192,6 +192,9 @@ def test_operator_applies_match_assembled_matrices():
     xv = x.copy()
     xv[0] = 0.0
     assert rel(sim.apply_operator("mom_v", xv).ravel(), Av @ xv.ravel()) <= 1e-13
+    from oracle.step import nutrient_system
+    An, _ = nutrient_system(st, st.phi, prm)
+    assert rel(sim.apply_operator("nutrient", x).ravel(), An @ x.ravel()) <= 1e-13
     sim.close()
 
 
@@ -352,6 +355,11 @@ def _solve_case(nx, ny, op, seed=0, **over):
         A = Au if op == "mom_u" else Av
         ref, it = cg(A, b.ravel(), x0.ravel(), 1.0 / A.diagonal(), prm.rtol, prm.maxit)
         sysname = "u" if op == "mom_u" else "v"
+    elif op == "nutrient":
+        from oracle.step import nutrient_system
+        A, _ = nutrient_system(s0, s0.phi, prm)
+        ref, it = cg(A, b.ravel(), x0.ravel(), 1.0 / A.diagonal(), prm.rtol, prm.maxit)
+        sysname = "nutrient"
     else:
         Mx, My = ex.mobility_faces(phs, prm.Lambda)
         A = asm.ch_matrix(nx, ny, prm.dt, prm.Gamma1, Mx, My, prm.theta_ch, prm.theta_adv,
@@ -393,7 +401,7 @@ def _check_momentum_solve(op, nx, ny, x, ref, it_gpu, it_ref, seed=0, **over):
     assert abs(it_gpu - it_ref) <= 2 + 0.05 * it_ref, (it_gpu, it_ref)
 
 
-@pytest.mark.parametrize("op", ["poisson", "mom_u", "mom_v", "ch"])
+@pytest.mark.parametrize("op", ["poisson", "mom_u", "mom_v", "ch", "nutrient"])
 @pytest.mark.parametrize("nx,ny", [(64, 48), (300, 37)])
 def test_isolated_solve_matches_oracle(op, nx, ny):
     """Same b, x0 and coefficients on both sides (see _check_momentum_solve for
