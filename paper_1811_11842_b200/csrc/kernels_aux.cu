@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(AP_T) k_op5_rm(Geom g, Op5T op, const double* 
   const int c0 = chunk * cw, wc = min(cw, g.nx - c0);
   const int n = jl1 - jl0, nq = n + 2;   // ring rows j0+jl0-1 .. j0+jl1
   const int rbase = g.j0 + jl0 - 1;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int t = threadIdx.x;
   const bool own = 2 * t < wc;
   const int ci = 2 * t + 2;
   if (t == 0) {
@@ -217,8 +217,6 @@ __global__ void __launch_bounds__(AP_T) k_op5_rm(Geom g, Op5T op, const double* 
       issue((r - 1) % AP_NST, r - 1 + AP_NST);
     }
   }
-  (void)lane;
-  (void)warp;
 }
 
 // ---------------------------------------------------------------- CG finish

@@ -119,16 +119,41 @@ __global__ void __launch_bounds__(RM_T) k_ch_rm(Geom g, ChCoef cc, const double*
     xb[j] = xh(slot(1), ci - 1 + j);
     wm[j] = wc_[j] = 0.0;
   }
-  const double L = cc.Lambda;
+  // face mobility Lambda max(0, (a + b)/2) = hL max(0, a + b), hL = Lambda/2 (exact: the
+  // factor 1/2 is a power of two); x/dt as x * (1/dt)
+  const double hL = 0.5 * cc.Lambda, idt = 1.0 / cc.dt;
   const bool adv = cc.u != nullptr;
-  // v on the south face of the current output row (row gj = rbase + k)
-  double2 vS2 = make_double2(0.0, 0.0);
-  if (adv && own) {
-    const int gj = rbase + 2;
-    if (gj > 0) vS2 = *reinterpret_cast<const double2*>(cc.v + off(g, gj, c0 + 2 * t));
-  }
+  // face velocities of the advection part, prefetched two output rows ahead in
+  // registers: u on the pair's three x-faces of row gj, v on its y-faces gj, gj + 1
+  // (v = 0 on the wall faces)
+  const int lastrow = rbase + n + 1;
+  struct UF {
+    double2 w;
+    double e;
+  };
+  auto ldu = [&](int gj) -> UF {
+    UF r{make_double2(0.0, 0.0), 0.0};
+    if (!adv || !own || gj > lastrow) return r;
+    const size_t o = off(g, gj, c0 + 2 * t);
+    r.w = __ldg(reinterpret_cast<const double2*>(cc.u + o));
+    const int ce = c0 + 2 * t + 2;
+    r.e = __ldg(cc.u + off(g, gj, ce >= g.nx ? ce - g.nx : ce));
+    return r;
+  };
+  auto ldv = [&](int gj) -> double2 {
+    if (!adv || !own || gj <= 0 || gj >= g.ny || gj > lastrow + 1) return make_double2(0.0, 0.0);
+    return __ldg(reinterpret_cast<const double2*>(cc.v + off(g, gj, c0 + 2 * t)));
+  };
+  UF uq0 = ldu(rbase + 2), uq1 = ldu(rbase + 3);
+  double2 vS2 = ldv(rbase + 2), vq0 = ldv(rbase + 3), vq1 = ldv(rbase + 4);
   double s0 = 0.0, s1 = 0.0;
   for (int k = 0; k <= n + 1; ++k) {
+    UF unew{make_double2(0.0, 0.0), 0.0};
+    double2 vnew = make_double2(0.0, 0.0);
+    if (k >= 2) {   // loads for output row rbase + k + 2 (two rows ahead)
+      unew = ldu(rbase + k + 2);
+      vnew = ldv(rbase + k + 3);
+    }
     wait_row(k + 2);
     // w on ring row k + 1 (x^ rows k, k+1, k+2) at columns c-1 .. c+2
     const double* sc1 = slot(k + 1);
@@ -150,23 +175,21 @@ __global__ void __launch_bounds__(RM_T) k_ch_rm(Geom g, ChCoef cc, const double*
       for (int j = 0; j < 2; ++j) {
         const int cc_ = ci + j;      // staged index of this column
         const double pc = ps1[cc_];
-        const double mE = L * fmax(0.0, 0.5 * (pc + ps1[cc_ + 1]));
-        const double mW = L * fmax(0.0, 0.5 * (pc + ps1[cc_ - 1]));
-        const double mN = (gj == g.ny - 1) ? 0.0 : L * fmax(0.0, 0.5 * (pc + ps2[cc_]));
-        const double mS = (gj == 0) ? 0.0 : L * fmax(0.0, 0.5 * (pc + ps0[cc_]));
+        const double mE = hL * fmax(0.0, pc + ps1[cc_ + 1]);
+        const double mW = hL * fmax(0.0, pc + ps1[cc_ - 1]);
+        const double mN = (gj == g.ny - 1) ? 0.0 : hL * fmax(0.0, pc + ps2[cc_]);
+        const double mS = (gj == 0) ? 0.0 : hL * fmax(0.0, pc + ps0[cc_]);
         const double w0 = wc_[j + 1];
         const double div = (mE * (wc_[j + 2] - w0) - mW * (w0 - wc_[j])) * g.ihx2 +
                            (mN * (wp[j + 1] - w0) - mS * (w0 - wm[j + 1])) * g.ihy2;
-        yv[j] = xa[j + 1] / cc.dt + cc.g1t * div;
+        yv[j] = xa[j + 1] * idt + cc.g1t * div;
       }
       const size_t o = off(g, gj, c0 + 2 * t);
       if (adv) {
         // ta Adv(x^) = ta [ (uE (x+xE) - uW (xW+x)) / 2hx + (vN (x+xN) - vS (xS+x)) / 2hy ]
-        const double2 uw = *reinterpret_cast<const double2*>(cc.u + o);
-        const int ce = c0 + 2 * t + 2;
-        const double ue = cc.u[off(g, gj, ce >= g.nx ? ce - g.nx : ce)];
-        const double2 vn = gj + 1 < g.ny ? *reinterpret_cast<const double2*>(cc.v + off(g, gj + 1, c0 + 2 * t))
-                                         : make_double2(0.0, 0.0);
+        const double2 uw = uq0.w;
+        const double ue = uq0.e;
+        const double2 vn = vq0;
         const double* xs0 = slot(k - 1);
         const double xS0 = xh(xs0, ci), xS1 = xh(xs0, ci + 1);
         const double hx = 0.5 * g.ihx, hy = 0.5 * g.ihy;
@@ -176,7 +199,6 @@ __global__ void __launch_bounds__(RM_T) k_ch_rm(Geom g, ChCoef cc, const double*
                           (vn.y * (xa[2] + xb[2]) - vS2.y * (xS1 + xa[2])) * hy;
         yv[0] += cc.tha * a0;
         yv[1] += cc.tha * a1;
-        vS2 = vn;
       }
       *reinterpret_cast<double2*>(y + o) = make_double2(yv[0], yv[1]);
       if (NDOT >= 1) {
@@ -203,6 +225,13 @@ __global__ void __launch_bounds__(RM_T) k_ch_rm(Geom g, ChCoef cc, const double*
       xb[j] = xn[j];
       wm[j] = wc_[j];
       wc_[j] = wp[j];
+    }
+    if (k >= 2) {   // the velocity FIFO advances with the output row
+      uq0 = uq1;
+      uq1 = unew;
+      vS2 = vq0;
+      vq0 = vq1;
+      vq1 = vnew;
     }
   }
   if (NDOT == 1) {

@@ -56,7 +56,7 @@ else:
     sim.enable_timing(a.stride)
     sim.step(a.steps)
 st = sim.stats()
-out = {"variant": os.environ.get("CHB_VEC", "default"), "defer": os.environ.get("CHB_DEFER", "32"),
+out = {"lib": os.environ.get("CHB_LIB", "default"), "defer": os.environ.get("CHB_DEFER", "64"),
        "solve": a.solve, "config": cfg["name"], "iters": st["iters_last"], "kernels": {}}
 if a.solve:
     out["solve_ms"] = solve_ms
