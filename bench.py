@@ -201,7 +201,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = kd["bytes"] / (kd["ms"] / 1e3) / 1e9 if kd["ms"] > 0 else None
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and nx == ny == 4096:   # the ncu captures are of the 4096^2 workload
         with open(tp) as fh:
             tr = json.load(fh).get(name)
         if tr:   # dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full)

@@ -42,7 +42,8 @@ def test_default_run_is_the_declared_workload():
 
 @pytest.mark.gpu
 def test_our_arm_line():
-    d = _line(["--config", "0", "--steps", "2", "--warmup", "3", "--no-cpu"])
+    d = _line(["--config", "0", "--steps", "2", "--warmup", "3", "--no-cpu",
+               "--matvec-sizes", "256", "512"])
     assert BASE_KEYS <= set(d), set(d) ^ BASE_KEYS
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3
     assert d["dtype"] == "f64" and d["higher_is_better"] is True
@@ -53,3 +54,6 @@ def test_our_arm_line():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    mv = d["matvec_sweep"]["records"]
+    assert {(r["op"], r["n"]) for r in mv} == {(o, n) for o in ("ch", "poisson") for n in (256, 512)}
+    assert all(r["GBps"] > 0 for r in mv)
