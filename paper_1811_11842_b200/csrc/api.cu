@@ -87,6 +87,9 @@ struct ch_handle {
   int cg3 = 1;                // single-reduction CG: three-term z recurrence (env CHB_CG3)
   int strip2 = 0;             // rows per strip, 0 = one resident wave (env CHB_STRIP)
   int pdl = 1;                // programmatic dependent launch of the CG sweeps (env CHB_PDL)
+  int ms = 1;                 // virtual slabs: one sweep launch over all slabs with in-kernel
+                              // halo rows and cross-slab finalize (env CHB_MS=0: per-slab
+                              // launches + halo copies + finalize kernel)
   int64_t tidx = 0;           // time index n of the state (ch_set_time_index; R23 start-up)
 };
 
@@ -219,6 +222,9 @@ RedArgs rargs(ch_handle* h, int fin, int sys, int slab) {
   ra.inline_fin = (h->nslabs_total == 1);
   ra.slab = slab;
   ra.pad = 0;
+  ra.nbs = 0;
+  ra.nslab = h->S;
+  ra.ticket2 = h->ticket + MS_MAX;
   return ra;
 }
 
@@ -507,6 +513,7 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
                                     8.0 * (m + 4) * (double)(K / m)) * cells;
   } else {
   const int tt = h->cg3 && NZ >= 3;
+  const bool ms_launch = h->ms && h->S > 1 && h->S <= MS_MAX && !h->comm;
   long k = 0;
   int chunk = 4;
   for (;;) {
@@ -516,16 +523,39 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
       // three-term: the sweep reads z_{k-1} (still in the ring) instead of s_{k-1}
       // and writes no s
       const int si = tt ? Zr[(k + NZ - 1) % NZ] : S[(k + 1) & 1], so = tt ? -1 : S[k & 1];
-      {
-        KTime kt(h, kc_sys, cgs_bytes(ekind, first, tt) * cells, k + 1);
+      if (ms_launch) {
+        // all local slabs in one launch: halo rows and the cross-slab finalize in-kernel
+        MsArgs ma;
+        memset(&ma, 0, sizeof ma);
+        ma.S = h->S;
         for (int s = 0; s < h->S; ++s) {
           Slab& sl = h->sl[s];
-          launch_cgs_iter(opdesc(h, kind, sl), sl.g, sl.a[zi], sl.a[zo], sl.a[si],
-                          so >= 0 ? sl.a[so] : nullptr, first, dir, tt,
-                          rargs(h, FIN_CGS, sys, s), h->st);
+          const OpDesc od = opdesc(h, kind, sl);
+          ma.g[s] = sl.g;
+          ma.zi[s] = sl.a[zi];
+          ma.zo[s] = sl.a[zo];
+          ma.si[s] = sl.a[si];
+          ma.so[s] = so >= 0 ? sl.a[so] : nullptr;
+          ma.w[s] = od.w;
+          ma.a[s] = od.a;
         }
+        KTime kt(h, kc_sys, cgs_bytes(ekind, first, tt) * cells, k + 1);
+        h->stats.launches -= h->S - 1;   // one launch for all slabs
+        h->stats.kc_launches[kc_sys] -= h->S - 1;
+        launch_cgs_iter_ms(opdesc(h, kind, h->sl[0]), ma, first, dir, tt,
+                           rargs(h, FIN_CGS, sys, 0), h->st);
+      } else {
+        {
+          KTime kt(h, kc_sys, cgs_bytes(ekind, first, tt) * cells, k + 1);
+          for (int s = 0; s < h->S; ++s) {
+            Slab& sl = h->sl[s];
+            launch_cgs_iter(opdesc(h, kind, sl), sl.g, sl.a[zi], sl.a[zo], sl.a[si],
+                            so >= 0 ? sl.a[so] : nullptr, first, dir, tt,
+                            rargs(h, FIN_CGS, sys, s), h->st);
+          }
+        }
+        TRY(iter_exchange(h, FIN_CGS, sys, 3, zo, so));
       }
-      TRY(iter_exchange(h, FIN_CGS, sys, 3, zo, so));
       if ((k + 1) % m == 0) TRY(px(k, m, 1));
     }
     TRY(check_launch(h, "cgs iteration"));
@@ -1094,6 +1124,7 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   if (const char* e = getenv("CHB_CG3")) h->cg3 = atoi(e) != 0;
   if (const char* e = getenv("CHB_STRIP")) h->strip2 = std::max(0, atoi(e));
   if (const char* e = getenv("CHB_PDL")) h->pdl = atoi(e) != 0;
+  if (const char* e = getenv("CHB_MS")) h->ms = atoi(e) != 0;
   if (const char* e = getenv("CHB_DEFER")) h->cg_defer = std::min(std::max(2, atoi(e)), CGM);
   if (const char* e = getenv("CHB_PERSIST")) h->persist = atoi(e) != 0;
   memset(&h->stats, 0, sizeof(ch_stats));
@@ -1151,7 +1182,7 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   if (cudaMalloc(&h->sc, NSC * sizeof(KScal)) != cudaSuccess ||
       cudaMallocHost(&h->sch, NSC * sizeof(KScal)) != cudaSuccess ||
       cudaMalloc(&h->part, (size_t)MAX_BLOCKS * 8 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&h->ticket, sizeof(unsigned int)) != cudaSuccess ||
+      cudaMalloc(&h->ticket, (MS_MAX + 1) * sizeof(unsigned int)) != cudaSuccess ||
       cudaMalloc(&h->tot, (size_t)total * 8 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&h->tot_local, (size_t)total * 8 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&h->gm_dev, 192 * sizeof(double)) != cudaSuccess ||
@@ -1162,7 +1193,7 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
     return fail(CH_ERR_CUDA, h, "cudaMalloc (scalars)");
   cudaMemset(h->sc, 0, NSC * sizeof(KScal));
   memset(h->sch, 0, NSC * sizeof(KScal));
-  cudaMemset(h->ticket, 0, sizeof(unsigned int));
+  cudaMemset(h->ticket, 0, (MS_MAX + 1) * sizeof(unsigned int));
   h->st = nullptr;
   // c = 1 initially
   {

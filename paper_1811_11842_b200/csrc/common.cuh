@@ -500,7 +500,7 @@ __device__ __forceinline__ void trace_pt(int i) {
 // total for a later cross-slab finalize.
 struct RedArgs {
   double* part;          // [nblocks * 8]
-  unsigned int* ticket;  // zeroed; reset by the last block
+  unsigned int* ticket;  // zeroed; reset by the last block (multi-slab launch: one per slab)
   double* tot;           // [nslabs_total * 8] slab totals (when !inline_fin)
   KScal* sc;
   FinCtx fc;
@@ -508,6 +508,12 @@ struct RedArgs {
   int inline_fin;
   int slab;              // index of this slab in tot
   int pad;
+  // one launch over several slabs (nbs > 0): blocks [s*nbs, (s+1)*nbs) are slab
+  // s, each slab's last block stores the slab total, the last slab to finish
+  // (ticket2) combines the totals in slab order and finalizes
+  int nbs;
+  int nslab;
+  unsigned int* ticket2;
 };
 
 template <int K>
@@ -518,8 +524,12 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
   const int tid = threadIdx.x + threadIdx.y * blockDim.x;
   const int lane = tid & 31, wid = tid >> 5;
   const int nw = (blockDim.x * blockDim.y + 31) >> 5;
-  const int bid = blockIdx.x + blockIdx.y * gridDim.x;
-  const int nb = gridDim.x * gridDim.y;
+  const int gbid = blockIdx.x + blockIdx.y * gridDim.x;
+  const int ms_slab = ra.nbs > 0 ? gbid / ra.nbs : ra.slab;
+  const int bid = ra.nbs > 0 ? gbid % ra.nbs : gbid;
+  const int nb = ra.nbs > 0 ? ra.nbs : gridDim.x * gridDim.y;
+  double* const part = ra.nbs > 0 ? ra.part + (size_t)ms_slab * ra.nbs * 8 : ra.part;
+  unsigned int* const ticket = ra.nbs > 0 ? ra.ticket + ms_slab : ra.ticket;
 #pragma unroll
   for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
   if (pre) CHB_TP(5);
@@ -533,7 +543,7 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
     for (int k = 0; k < K; ++k) {
       double t = lane < nw ? sm[lane][k] : 0.0;
       t = warp_sum(t);
-      if (lane == 0) ra.part[(size_t)bid * 8 + k] = t;
+      if (lane == 0) part[(size_t)bid * 8 + k] = t;
     }
     if (lane == 0) {
       // acq_rel ticket: releases this CTA's partials; the last arrival
@@ -541,7 +551,7 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
       // Replaces __threadfence() (MEMBAR.SC.GPU + L1 invalidate) on both sides.
       unsigned prev;
       asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
-                   : "=r"(prev) : "l"(ra.ticket) : "memory");
+                   : "=r"(prev) : "l"(ticket) : "memory");
       am_last = (prev == (unsigned)(nb - 1));
     }
   }
@@ -567,7 +577,7 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
       for (int u = 0; u < U; ++u) {
         const int b = b0 + u * nthr;
 #pragma unroll
-        for (int k = 0; k < K; ++k) x[u][k] = b < nb ? __ldcg(ra.part + (size_t)b * 8 + k) : 0.0;
+        for (int k = 0; k < K; ++k) x[u][k] = b < nb ? __ldcg(part + (size_t)b * 8 + k) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -590,17 +600,54 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
     for (int w = 0; w < nw; ++w) t += sm[w][k];
     res[k] = t;
   }
-  if (lane == 0) *ra.ticket = 0u;
+  if (lane == 0) *ticket = 0u;
   if (ra.inline_fin) {
     if (pre && ra.fin == FIN_CGS)
       finalize_cgs_pre(res, *pre, slot, ra.sc, ra.fc, lane);
     else
       finalize_warp(ra.fin, res, ra.sc, ra.fc);
+  } else if (ra.nbs > 0) {
+    // multi-slab launch: store this slab's total; the last slab combines
+    unsigned prev = 0;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) ra.tot[ms_slab * 8 + k] = res[k];
+      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                   : "=r"(prev) : "l"(ra.ticket2) : "memory");
+    }
+    prev = __shfl_sync(FULL, prev, 0);
+    if (prev != (unsigned)(ra.nslab - 1)) return;
+    double t[8];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double a = 0.0;
+      for (int s = 0; s < ra.nslab; ++s) a += __ldcg(ra.tot + s * 8 + k);   // slab order
+      t[k] = a;
+    }
+    if (lane == 0) *ra.ticket2 = 0u;
+    finalize_warp(ra.fin, t, ra.sc, ra.fc);
   } else if (lane == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) ra.tot[ra.slab * 8 + k] = res[k];
   }
 }
+
+// Per-slab arguments of one CG sweep launch over all local slabs (virtual
+// slabs of one process): the sweep of slab s stores its first / last two rows
+// of z' (and s) also into the ghost rows of slab s-1 / s+1 -- the halo
+// exchange happens inside the sweep, no copies, no extra launches.
+constexpr int MS_MAX = 8;
+struct MsArgs {
+  int S;     // slabs in the launch (0 or 1: single-slab launch)
+  int nbs;   // blocks per slab
+  Geom g[MS_MAX];
+  const double* zi[MS_MAX];
+  double* zo[MS_MAX];
+  const double* si[MS_MAX];
+  double* so[MS_MAX];
+  const double* w[MS_MAX];
+  const double* a[MS_MAX];
+};
 
 // Cross-slab finalize: sums slab totals in slab order, then finalizes.
 __global__ void k_finalize_slabs(const double* tot, int nslabs, int K, RedArgs ra);

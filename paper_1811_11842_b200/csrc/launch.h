@@ -39,6 +39,10 @@ void launch_cg5_finish(const Geom& g, double* x, const double* p, int nullspace,
 void launch_cgs_iter(const OpDesc& d, const Geom& g, const double* zi, double* zo,
                      const double* si, double* so, int first, int dir, int tt, const RedArgs& ra,
                      cudaStream_t st);
+// one sweep launch over all local slabs (halo rows stored into the neighbours'
+// ghost rows, cross-slab finalize by the last slab), common.cuh MsArgs
+void launch_cgs_iter_ms(const OpDesc& d, const MsArgs& ms, int first, int dir, int tt,
+                        const RedArgs& ra, cudaStream_t st);
 struct ZList {
   const double* z[CGM];
 };

@@ -119,17 +119,22 @@ def test_odd_nx_rejected():
         Simulation(45, 38)
 
 
+@pytest.mark.parametrize("ms", ["1", "0"])
 @pytest.mark.parametrize("cg3", ["1", "0"])
 @pytest.mark.parametrize("slabs", [2, 3])
-def test_virtual_slabs_match_single_slab(slabs, cg3, monkeypatch):
+def test_virtual_slabs_match_single_slab(slabs, cg3, ms, monkeypatch):
     """Slab decomposition in y with halo exchange reproduces the 1-slab step
     (CG: three-term z recurrence, z halos only; and s recurrence, z + s
-    halos).  Dot products sum in a different order per decomposition, so the
-    solves run to rtol 1e-13 (differences are rounding propagated through the
-    CG iterations, not solver tolerance)."""
+    halos), with the CG iteration as ONE launch over all slabs (ms = 1: the
+    sweep stores its slab-edge rows into the neighbours' ghost rows and the
+    last slab combines the partial sums) or as per-slab launches + halo copies
+    + a finalize kernel (ms = 0, the multi-rank code path).  Dot products sum
+    in a different order per decomposition, so the solves run to rtol 1e-13
+    (differences are rounding propagated through the CG iterations)."""
     from paper_1811_11842_b200 import Simulation
     from workloads import initial_fields
     monkeypatch.setenv("CHB_CG3", cg3)
+    monkeypatch.setenv("CHB_MS", ms)
     f = initial_fields(40, 36, seed=4)
     u, v = stream_velocity(40, 36, seed=2, scale=0.01)
     f["u"], f["v"] = u, v
@@ -257,6 +262,23 @@ def test_mass_conserved_and_divergence_free_on_gpu():
 
 
 # ----------------------------------------- production launch geometry (strips)
+@pytest.mark.parametrize("slabs", [3])
+@pytest.mark.parametrize("strip", ["2", "12"])
+def test_virtual_slabs_forced_strips(strip, slabs, monkeypatch):
+    """One-launch multi-slab sweep with forced strip heights (slab-edge rows
+    inside and at the ends of strips) on a ragged 300 x 200 grid, all operator
+    kinds, against the oracle."""
+    from workloads import initial_fields
+    monkeypatch.setenv("CHB_STRIP", strip)
+    nx, ny = 300, 200
+    f = initial_fields(nx, ny, seed=9)
+    f["u"], f["v"] = stream_velocity(nx, ny, seed=9, scale=0.01)
+    got, ref, st, iters = run_both(nx, ny, 2, slabs=slabs, fields=f, rtol=1e-12, rho_n=1.2,
+                                   Lambda=1e-6)
+    for k in FIELDS:
+        assert rel(got[k], ref[k]) <= 1e-9, (strip, k, rel(got[k], ref[k]))
+
+
 @pytest.mark.parametrize("strip", ["1", "2", "3", "12", "40"])
 def test_forced_strips_all_operator_kinds(strip, monkeypatch):
     """Forced strip heights at ~300 x 200 (two column chunks, one ragged): the
