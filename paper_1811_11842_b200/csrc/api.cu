@@ -779,17 +779,21 @@ int step_once(ch_handle* h) {
   TRY(check_launch(h, "div"));
   TRY(fin_slabs(h, FIN_MEAN, CH_SYS_P, 1));
   const int pk = (h->prm.rho_n == h->prm.rho_s) ? OPK_POISSON_CONST : OPK_POISSON_VAR;
-  TRY(cg_any(h, CH_SYS_P, pk, A_P, A_B, 1, 1, "pressure", pk == OPK_POISSON_VAR ? A_PHI1 : -1));
+  // p^{n+1} into a work array (initial guess p^n), so that a failed solve leaves p^n
+  TRY(copy_arr(h, A_P, A_TMP2));
+  TRY(cg_any(h, CH_SYS_P, pk, A_TMP2, A_B, 1, 1, "pressure",
+             pk == OPK_POISSON_VAR ? A_PHI1 : -1));
   {
     KTime kt(h, CH_KC_VEC, 16.0 * cells);
-    for (auto& s : h->sl) launch_sub_mean(s.g, s.a[A_P], h->sc + CH_SYS_P, h->st);
+    for (auto& s : h->sl) launch_sub_mean(s.g, s.a[A_TMP2], h->sc + CH_SYS_P, h->st);
   }
-  // 5. projection
-  TRY(halo(h, A_P, 1));
+  // 5. projection (every solve has succeeded: the state is updated from here on)
+  TRY(halo(h, A_TMP2, 1));
   {
     KTime kt(h, CH_KC_RHS, 56.0 * cells);
     for (auto& s : h->sl)
-      launch_project(s.g, ph, s.a[A_PHI1], s.a[A_US], s.a[A_VS], s.a[A_P], s.a[A_U], s.a[A_V], h->st);
+      launch_project(s.g, ph, s.a[A_PHI1], s.a[A_US], s.a[A_VS], s.a[A_TMP2], s.a[A_U], s.a[A_V],
+                     h->st);
   }
   TRY(check_launch(h, "project"));
   // rotate time levels
@@ -797,6 +801,7 @@ int step_once(ch_handle* h) {
     std::swap(s.a[A_PHIP], s.a[A_PHI]);   // phi_prev <- phi^n
     std::swap(s.a[A_PHI], s.a[A_PHI1]);   // phi <- phi^{n+1}
     std::swap(s.a[A_C], s.a[A_C1]);
+    std::swap(s.a[A_P], s.a[A_TMP2]);     // p <- p^{n+1}
   }
   harvest(h, -1);
   h->stats.steps += 1;

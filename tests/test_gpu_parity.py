@@ -464,3 +464,32 @@ def test_persistent_isolated_solve(op, monkeypatch):
     else:
         assert rel(x, ref) <= 1e-9, (op, rel(x, ref))
         assert abs(it_gpu - it_ref) <= 2, (it_gpu, it_ref)
+
+
+def test_not_converged_is_reported_with_the_system_and_residual():
+    """A solve hitting maxit raises CH_ERR_NOT_CONVERGED naming the system, the
+    iteration count and the residual reached; the state stays at the last
+    completed step (here: the initial condition)."""
+    from paper_1811_11842_b200 import CHError, Simulation
+    from workloads import initial_fields
+    f = initial_fields(64, 64, seed=1)
+    sim = Simulation(64, 64, maxit=5)
+    sim.set_fields(**f)
+    with pytest.raises(CHError) as ei:
+        sim.step(1)
+    msg = str(ei.value)
+    assert ei.value.code == 3 and "not converged in 5 iterations" in msg, msg
+    assert sim.time_index == 0
+    for k in FIELDS:
+        assert np.array_equal(sim.get_field(k), f[k]), k
+    # a pressure solve that fails leaves p^n as well (the CH, nutrient and
+    # momentum solves are cheap at 64^2 with maxit high enough for them)
+    sim.close()
+    sim = Simulation(64, 64, maxit=100)
+    sim.set_fields(**f)
+    with pytest.raises(CHError) as ei:
+        sim.step(1)
+    assert "pressure" in str(ei.value) or "momentum" in str(ei.value), str(ei.value)
+    for k in FIELDS:
+        assert np.array_equal(sim.get_field(k), f[k]), k
+    sim.close()
