@@ -110,8 +110,13 @@ __global__ void __launch_bounds__(RM_T) k_ch_rm(Geom g, ChCoef cc, const double*
   auto wait_row = [&](int q) {
     mbar_wait_s(bars_s + 8u * (uint32_t)(q % RM_NST), (uint32_t)((q / RM_NST) & 1));
   };
-  // x^ rows (older -> newer) at columns c-1 .. c+2 of the thread's pair
+  // x^ rows (older -> newer) at columns c-1 .. c+2 of the thread's pair; w = Delta_h x^
+  // at the pair's own columns in registers (wm, wc_, wp: rows k-1, k, k+1, indices
+  // 1..2), the neighbours' from a 3-row shared buffer (each w computed once; the
+  // chunk's halo columns by the first / last owning thread)
+  __shared__ double wrow[3][RM_SEG];
   double xa[4], xb[4], wm[4], wc_[4], wp[4];
+  const bool edgeL = own && t == 0, edgeR = own && 2 * t + 2 >= wc;
   wait_row(0);
   wait_row(1);
   for (int j = 0; j < 4; ++j) {
@@ -160,14 +165,27 @@ __global__ void __launch_bounds__(RM_T) k_ch_rm(Geom g, ChCoef cc, const double*
     const double* sc2 = slot(k + 2);
     double xn[4];
     for (int j = 0; j < 4; ++j) xn[j] = xh(sc2, ci - 1 + j);
-    const double xl = xh(sc1, ci - 2), xr = xh(sc1, ci + 3);
-    for (int j = 0; j < 4; ++j) {
-      const double xw = j == 0 ? xl : xb[j - 1], xe = j == 3 ? xr : xb[j + 1];
-      wp[j] = (xe - 2.0 * xb[j] + xw) * g.ihx2 + (xn[j] - 2.0 * xb[j] + xa[j]) * g.ihy2;
+    for (int j = 1; j <= 2; ++j)
+      wp[j] = (xb[j + 1] - 2.0 * xb[j] + xb[j - 1]) * g.ihx2 +
+              (xn[j] - 2.0 * xb[j] + xa[j]) * g.ihy2;
+    if (own) {
+      double* wr = wrow[(k + 1) % 3];
+      wr[ci] = wp[1];
+      wr[ci + 1] = wp[2];
+      if (edgeL) {
+        const double xl = xh(sc1, ci - 2);
+        wr[ci - 1] = (xb[1] - 2.0 * xb[0] + xl) * g.ihx2 + (xn[0] - 2.0 * xb[0] + xa[0]) * g.ihy2;
+      }
+      if (edgeR) {
+        const double xr = xh(sc1, ci + 3);
+        wr[ci + 2] = (xr - 2.0 * xb[3] + xb[2]) * g.ihx2 + (xn[3] - 2.0 * xb[3] + xa[3]) * g.ihy2;
+      }
     }
     // y on ring row k (owned rows 2 .. n+1): w rows k-1 (wm), k (wc_), k+1 (wp)
     if (k >= 2 && own) {
       const int gj = rbase + k;
+      wc_[0] = wrow[k % 3][ci - 1];   // row k's w at the neighbour columns (previous iteration)
+      wc_[3] = wrow[k % 3][ci + 2];
       const double* ps0 = slot(k - 1) + 2 * RM_SEG;
       const double* ps1 = slot(k) + 2 * RM_SEG;
       const double* ps2 = slot(k + 1) + 2 * RM_SEG;
@@ -223,6 +241,8 @@ __global__ void __launch_bounds__(RM_T) k_ch_rm(Geom g, ChCoef cc, const double*
     for (int j = 0; j < 4; ++j) {
       xa[j] = xb[j];
       xb[j] = xn[j];
+    }
+    for (int j = 1; j <= 2; ++j) {
       wm[j] = wc_[j];
       wc_[j] = wp[j];
     }
