@@ -222,23 +222,24 @@ def run_ours(args, rank, world, local_rank):
     # end-to-end through the public API with host buffers (rank-local slab)
     e2e = None
     if not args.no_e2e:
+        # the whole state: fields, phi^{n-1} and the momentum guesses u*, v* (R25)
+        extra = ("phi_prev", "u_star", "v_star")
         host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory().numpy() for k, v in
-                sim.get_fields(("phi", "c", "u", "v", "p")).items()}
-        hprev = torch.from_numpy(sim.get_field("phi_prev")).pin_memory().numpy()
+                sim.get_fields(("phi", "c", "u", "v", "p") + extra).items()}
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            sim.set_fields(**host)
-            sim.set_field("phi_prev", hprev)
+            sim.set_fields(**{k: host[k] for k in ("phi", "c", "u", "v", "p")})
+            for k in extra:
+                sim.set_field(k, host[k])
             sim.step(1)
             for k in host:
                 sim.get_field(k, host[k])
-            sim.get_field("phi_prev", hprev)
         barrier()
         dt = time.perf_counter() - t0
         dt_max = max_over_ranks(dist, dt, device="cuda")
-        nbytes = 6 * sim.nrows * nx * 8
+        nbytes = len(host) * sim.nrows * nx * 8
         e2e = {"value": e2e_steps / dt_max, "unit": "time-steps/s",
                "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world}
 

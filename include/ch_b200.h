@@ -62,7 +62,10 @@ enum {
   CH_FIELD_C = 2,         /* nutrient c (cells)                           */
   CH_FIELD_U = 3,         /* x-velocity (x-faces)                         */
   CH_FIELD_V = 4,         /* y-velocity (y-faces, row 0 = wall)           */
-  CH_FIELD_P = 5          /* pressure variable of Eq. 20 (cells, R15)     */
+  CH_FIELD_P = 5,         /* pressure variable of Eq. 20 (cells, R15)     */
+  CH_FIELD_U_STAR = 6,    /* u* of the last step = initial guess of the   */
+  CH_FIELD_V_STAR = 7     /* next momentum solves (R25; x-/y-   */
+                          /* faces); reset to u / v when u / v are set    */
 };
 
 /* Linear systems, in solve order within a step (also the stats index). */
@@ -193,7 +196,10 @@ int ch_get_time_index(const ch_handle* h, int64_t* n);
 
 /* Set the state (any pointer may be NULL = leave unchanged).  Each array is
  * the local slab, nrows x nx, ld = nx.  Setting phi also sets phi_prev = phi
- * (first step extrapolates to phi* = phi^0, R5). */
+ * (first step extrapolates to phi* = phi^0, R5); setting u (v) also
+ * sets the momentum guess u* (v*) to it (R25).  ch_set_field sets one field
+ * (CH_FIELD_*): the same side effects except for phi (PHI_PREV is its own
+ * field); U_STAR / V_STAR restore a saved guess and must follow u / v. */
 int ch_set_fields(ch_handle* h, const double* phi, const double* c, const double* u,
                   const double* v, const double* p, int where);
 int ch_set_field(ch_handle* h, int field, const double* src, int where);
@@ -204,7 +210,8 @@ int ch_set_field(ch_handle* h, int field, const double* src, int where);
  *      line with Eq. 4-5; theta-weighted Gamma1 term and advection, CN by
  *      default) solved by BiCGStab / GMRES(m) with Jacobi;
  *   2. nutrient c^{n+1} (Eq. 16 3rd line, Eq. 7), Jacobi-PCG;
- *   3. intermediate velocity u*, v* (Eq. 18-19, R6-R7), Jacobi-PCG each;
+ *   3. intermediate velocity u*, v* (Eq. 18-19, R6-R7), Jacobi-PCG each,
+ *      initial guesses the previous step's u*, v* (R25);
  *   4. pressure -div(1/rho grad p) = div u* (Eq. 20) with the constant null
  *      space removed (Listing 5), Jacobi-PCG;
  *   5. projection v^{n+1} = u* + (1/rho) grad p (Eq. 21).

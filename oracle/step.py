@@ -25,10 +25,21 @@ class State:
     v: np.ndarray          # y-velocity on y-faces (row 0 = bottom wall = 0)
     p: np.ndarray          # pressure (paper's Eq. 20 variable, Δt absorbed; R15)
     n: int = 0
+    us: np.ndarray | None = None   # u* of the previous step: initial guess of the
+    vs: np.ndarray | None = None   # next momentum solves (R25); None -> u, v
 
     def copy(self) -> "State":
         return State(self.phi.copy(), self.phi_prev.copy(), self.c.copy(),
-                     self.u.copy(), self.v.copy(), self.p.copy(), self.n)
+                     self.u.copy(), self.v.copy(), self.p.copy(), self.n,
+                     None if self.us is None else self.us.copy(),
+                     None if self.vs is None else self.vs.copy())
+
+    def guess_uv(self):
+        """Initial guesses of the momentum solves (R25): the previous step's
+        intermediate velocity (u*, v*), or (u, v) when there is none (the
+        first step after an initial condition is set)."""
+        return (self.u if self.us is None else self.us,
+                self.v if self.vs is None else self.vs)
 
 
 @dataclass
@@ -146,10 +157,11 @@ def step(st: State, prm: Params) -> tuple[State, StepInfo]:
     A, b = nutrient_system(st, phi1, prm)
     c1, info.iters["nutrient"] = cg(A, b, st.c.ravel(), 1.0 / A.diagonal(), prm.rtol, prm.maxit)
     c1 = c1.reshape(ny, nx)
-    # 3. intermediate velocity (u*, v*); guesses u^n, v^n
+    # 3. intermediate velocity (u*, v*); guesses u*, v* of the previous step (R25)
     (Au, bu), (Av, bv) = momentum_systems(st, phs, prm)
-    us, info.iters["u"] = cg(Au, bu, st.u.ravel(), 1.0 / Au.diagonal(), prm.rtol, prm.maxit)
-    vs, info.iters["v"] = cg(Av, bv, st.v.ravel(), 1.0 / Av.diagonal(), prm.rtol, prm.maxit)
+    gu, gv = st.guess_uv()
+    us, info.iters["u"] = cg(Au, bu, gu.ravel(), 1.0 / Au.diagonal(), prm.rtol, prm.maxit)
+    vs, info.iters["v"] = cg(Av, bv, gv.ravel(), 1.0 / Av.diagonal(), prm.rtol, prm.maxit)
     us, vs = us.reshape(ny, nx), vs.reshape(ny, nx)
     # 4. pressure Poisson (Eq. 20) with constant null space removed; guess p^n
     bx, by = ex.pressure_faces(phi1, prm.rho_n, prm.rho_s)
@@ -161,7 +173,8 @@ def step(st: State, prm: Params) -> tuple[State, StepInfo]:
     # 5. projection (Eq. 21)
     u1, v1 = ex.correct(us, vs, p1, bx, by)
     info.div_max = float(np.abs(ex.divergence(u1, v1)).max())
-    new = State(phi=phi1, phi_prev=st.phi.copy(), c=c1, u=u1, v=v1, p=p1, n=st.n + 1)
+    new = State(phi=phi1, phi_prev=st.phi.copy(), c=c1, u=u1, v=v1, p=p1, n=st.n + 1,
+                us=us, vs=vs)
     return new, info
 
 

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("CHB_LIB") or os.path.join(HERE, "libch_b200.so")  # o
 
 CH_OK, CH_ERR_ARG, CH_ERR_CUDA, CH_ERR_NOT_CONVERGED, CH_ERR_BREAKDOWN, CH_ERR_COMM = range(6)
 CH_HOST, CH_DEVICE = 0, 1
-FIELDS = {"phi": 0, "phi_prev": 1, "c": 2, "u": 3, "v": 4, "p": 5}
+FIELDS = {"phi": 0, "phi_prev": 1, "c": 2, "u": 3, "v": 4, "p": 5, "u_star": 6, "v_star": 7}
 SYSTEMS = ("ch", "nutrient", "u", "v", "p")
 OPS = {"ch": 0, "poisson": 1, "mom_u": 2, "mom_v": 3, "nutrient": 4}
 SOLVERS = {"bicgstab": 0, "gmres": 1}

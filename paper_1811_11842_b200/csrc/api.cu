@@ -26,6 +26,7 @@ enum Arr {
   A_Z, A_PA, A_PB,                         // CG
   A_R, A_RH, A_BP, A_BV, A_BS, A_BT,       // BiCGStab
   A_TMP, A_TMP2,
+  A_USG, A_VSG,                            // u*, v* of the last step: momentum guesses (R25)
   A_ZH0,                                   // z history of the deferred-p/x CG (CGM - 1 more)
   A_N = A_ZH0 + CGM - 1
 };
@@ -756,7 +757,7 @@ int step_once(ch_handle* h) {
       launch_mom_rhs_u(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_CW], s.a[A_B], h->st);
   }
   TRY(check_launch(h, "mom_rhs_u"));
-  TRY(copy_arr(h, A_U, A_US));
+  TRY(copy_arr(h, A_USG, A_US));  // initial guess u* of the previous step (R25)
   TRY(cg_any(h, CH_SYS_U, OPK_MOM_U, A_US, A_B, 0, 0, "momentum-u", A_CW));
   {
     KTime kt(h, CH_KC_RHS, 40.0 * cells);
@@ -764,7 +765,7 @@ int step_once(ch_handle* h) {
       launch_mom_rhs_v(s.g, ph, state(s), s.a[A_PHIS], s.a[A_CA], s.a[A_CW], s.a[A_B], h->st);
   }
   TRY(check_launch(h, "mom_rhs_v"));
-  TRY(copy_arr(h, A_V, A_VS));
+  TRY(copy_arr(h, A_VSG, A_VS));
   TRY(cg_any(h, CH_SYS_V, OPK_MOM_V, A_VS, A_B, 0, 0, "momentum-v", A_CW));
   // 4. pressure Poisson with the constant null space
   TRY(halo(h, A_US, 1));
@@ -802,6 +803,8 @@ int step_once(ch_handle* h) {
     std::swap(s.a[A_PHI], s.a[A_PHI1]);   // phi <- phi^{n+1}
     std::swap(s.a[A_C], s.a[A_C1]);
     std::swap(s.a[A_P], s.a[A_TMP2]);     // p <- p^{n+1}
+    std::swap(s.a[A_USG], s.a[A_US]);     // next step's momentum guesses <- u*, v* (R25)
+    std::swap(s.a[A_VSG], s.a[A_VS]);
   }
   harvest(h, -1);
   h->stats.steps += 1;
@@ -818,6 +821,8 @@ int field_arr(int field) {
     case CH_FIELD_U: return A_U;
     case CH_FIELD_V: return A_V;
     case CH_FIELD_P: return A_P;
+    case CH_FIELD_U_STAR: return A_USG;
+    case CH_FIELD_V_STAR: return A_VSG;
   }
   return -1;
 }
@@ -847,10 +852,10 @@ int get(ch_handle* h, int id, double* dst, int where) {
   return CH_OK;
 }
 
-int zero_vrow0(ch_handle* h) {
+int zero_vrow0(ch_handle* h, int id = A_V) {
   if (h->row0 == 0) {
     Slab& s = h->sl.front();
-    CK(cudaMemsetAsync(s.a[A_V] + (size_t)GH * s.g.pitch, 0, s.g.pitch * sizeof(double), h->st));
+    CK(cudaMemsetAsync(s.a[id] + (size_t)GH * s.g.pitch, 0, s.g.pitch * sizeof(double), h->st));
   }
   return CH_OK;
 }
@@ -1242,6 +1247,11 @@ int ch_set_field(ch_handle* h, int field, const double* src, int where) {
   }
   TRY(put(h, id, src, where));
   if (field == CH_FIELD_V) TRY(zero_vrow0(h));
+  // a new velocity resets the momentum guess to it (R25; oracle initial_state)
+  if (field == CH_FIELD_U) TRY(copy_arr(h, A_U, A_USG));
+  if (field == CH_FIELD_V) TRY(copy_arr(h, A_V, A_VSG));
+  if (field == CH_FIELD_V_STAR) TRY(zero_vrow0(h, A_VSG));
+  if (where != CH_DEVICE) CK(cudaStreamSynchronize(h->st));
   return CH_OK;
 }
 
@@ -1253,10 +1263,14 @@ int ch_set_fields(ch_handle* h, const double* phi, const double* c, const double
     TRY(copy_arr(h, A_PHI, A_PHIP));
   }
   if (c) TRY(put(h, A_C, c, where));
-  if (u) TRY(put(h, A_U, u, where));
+  if (u) {
+    TRY(put(h, A_U, u, where));
+    TRY(copy_arr(h, A_U, A_USG));  // momentum guess := u (R25)
+  }
   if (v) {
     TRY(put(h, A_V, v, where));
     TRY(zero_vrow0(h));
+    TRY(copy_arr(h, A_V, A_VSG));
   }
   if (p) TRY(put(h, A_P, p, where));
   if (where != CH_DEVICE) CK(cudaStreamSynchronize(h->st));

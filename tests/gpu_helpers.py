@@ -52,7 +52,7 @@ def run_both(nx, ny, steps, seed=0, slabs=1, fields=None, **over):
     sim = Simulation(nx, ny, sp, virtual_slabs=slabs)
     sim.set_fields(**f)
     sim.step(steps)
-    got = sim.get_fields()
+    got = sim.get_fields(FIELDS + ("u_star", "v_star"))
     st = sim.stats()
     sim.close()
     ost = initial_state(f)
@@ -61,5 +61,6 @@ def run_both(nx, ny, steps, seed=0, slabs=1, fields=None, **over):
     for _ in range(steps):
         ost, info = step(ost, prm)
         iters.append(info.iters)
-    ref = dict(phi=ost.phi, c=ost.c, u=ost.u, v=ost.v, p=ost.p)
+    gu, gv = ost.guess_uv()   # u*, v* of the last step (R25)
+    ref = dict(phi=ost.phi, c=ost.c, u=ost.u, v=ost.v, p=ost.p, u_star=gu, v_star=gv)
     return got, ref, st, iters

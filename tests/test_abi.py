@@ -66,3 +66,15 @@ def test_bad_arguments_rejected_before_device_work():
         Simulation(16, 16, theta_visc=0.0)
     with pytest.raises(CHError):
         Simulation(16, 16, dt=-1.0)
+
+
+def test_field_ids_match_header(tmp_path):
+    from paper_1811_11842_b200 import _lib
+    names = ["PHI", "PHI_PREV", "C", "U", "V", "P", "U_STAR", "V_STAR"]
+    src = tmp_path / "f.c"
+    src.write_text('#include "ch_b200.h"\n#include <stdio.h>\nint main(void){'
+                   + "".join(f'printf("%d\\n", CH_FIELD_{n});' for n in names) + "return 0;}\n")
+    exe = tmp_path / "f"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert vals == [_lib.FIELDS[n.lower()] for n in names]

@@ -39,3 +39,33 @@ def test_r22_three_term_z_recurrence_keeps_cg_accuracy():
     assert np.linalg.norm(x2 - xh) <= 1e-8 * np.linalg.norm(xh)
     assert r2 <= 3 * rh + 1e-10, (rh, r2)
     assert r3 > 10 * rh, (rh, r3)  # why x stays on the two-term update
+
+
+def test_r25_momentum_guess_is_the_previous_intermediate_velocity():
+    """R25 (oracle): the momentum solves of a step start from the previous
+    step's u*, v*.  Started from u^n instead, the same systems reach the same
+    solution (to the stopping point) but from a larger initial residual: the
+    projected u^n differs from u* by the pressure-gradient correction of
+    Eq. 21, the previous u* only by one step's change."""
+    import sys
+    sys.path.insert(0, ROOT)
+    from oracle import Params, initial_state, step
+    from oracle.krylov import cg
+    from oracle.step import ch_system, momentum_systems
+    from workloads import initial_fields
+    prm = Params(rtol=1e-12)
+    st = initial_state(initial_fields(32, 32, seed=1))
+    assert st.us is None and st.guess_uv()[0] is st.u
+    for _ in range(3):
+        st, _ = step(st, prm)
+    assert st.us is not None
+    _, _, phs = ch_system(st, prm)
+    (Au, bu), _ = momentum_systems(st, phs, prm)
+    dinv = 1.0 / Au.diagonal()
+    r_prev = np.linalg.norm(bu - Au @ st.us.ravel())
+    r_un = np.linalg.norm(bu - Au @ st.u.ravel())
+    assert r_prev < 0.1 * r_un, (r_prev, r_un)
+    x1, k1 = cg(Au, bu, st.us.ravel(), dinv, 1e-12, 10 ** 5)
+    x2, k2 = cg(Au, bu, st.u.ravel(), dinv, 1e-12, 10 ** 5)
+    assert k1 < k2, (k1, k2)
+    assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x2)
