@@ -169,9 +169,19 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status);
 
 /* Multi-process runs (grid->nranks > 1): join the NCCL clique.  `id` is the
  * 128-byte ncclUniqueId produced by rank 0 with ch_comm_unique_id and
- * broadcast by the caller (e.g. torch.distributed).  Collective. */
+ * broadcast by the caller (e.g. torch.distributed).  Collective.  Then, if
+ * every rank is its own process on its own device with peer access to all
+ * the others (and env CHB_P2P is not 0), maps the neighbours' CG ring arrays
+ * and every rank's reduction area through CUDA IPC: each CG iteration is then
+ * ONE kernel per rank that stores its edge rows of z' into the neighbours'
+ * ghost rows and combines the iteration's inner products over NVLink peer
+ * memory ("MPI is used to communicate ghost points"; DESIGN.md
+ * §7).  Also makes the deferred-p/x block length the minimum over ranks. */
 int ch_comm_unique_id(void* id_out, size_t len);
 int ch_comm_init(ch_handle* h, const void* id, size_t len);
+/* 0: single process; 1: NCCL halo rows + allgather per CG iteration;
+ * 2: peer-memory CG iterations (NCCL for the rest of the step). */
+int ch_comm_mode(const ch_handle* h);
 
 /* Rows owned by this handle: [*row0, *row0 + *nrows). */
 int ch_local_rows(const ch_handle* h, int32_t* row0, int32_t* nrows);
@@ -249,6 +259,19 @@ int ch_reset_stats(ch_handle* h);
 /* Sample every `stride`-th launch of each kernel class with a CUDA event pair
  * on the library stream (0 = off). */
 int ch_enable_timing(ch_handle* h, int stride);
+
+/* Self-test of the peer-memory combine of the CG sweep on one
+ * device: `nranks` groups of `nloc` CTAs play the ranks of a clique inside ONE
+ * cooperative launch (the way blocks that wait on one another may share a
+ * GPU), each with its own totals area and flags, for `epochs` iterations with
+ * randomised arrival order; at epoch `absent_epoch` (0 = never) the last rank
+ * does not arrive and every other rank must time out (~2 s) instead of
+ * hanging.  Returns the number of mismatches (0: every rank computed the
+ * bit-exact slab-ordered sums, every timeout was reported) or -CH_ERR_*.
+ * last (may be NULL): [nranks][8] combined totals of the last epoch.
+ * nranks <= 8, nloc <= 8. */
+int ch_selftest_xrank(int device, int nranks, int nloc, int epochs, int absent_epoch,
+                      double* last);
 
 const char* ch_last_error(const ch_handle* h);
 int ch_abi_version(void);

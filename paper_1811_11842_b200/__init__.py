@@ -114,6 +114,12 @@ class Simulation:
     def comm_init(self, uid: bytes):
         self._check(lib.ch_comm_init(self._h, uid, len(uid)))
 
+    @property
+    def comm_mode(self) -> str:
+        """"single" (one process), "nccl" (NCCL group per CG iteration) or
+        "p2p" (peer-memory CG iterations, ch_comm_mode)."""
+        return {0: "single", 1: "nccl", 2: "p2p"}[lib.ch_comm_mode(self._h)]
+
     def set_stream(self, stream):
         """stream: torch.cuda.Stream, raw cudaStream_t int, or None (legacy default)."""
         ptr = getattr(stream, "cuda_stream", stream)

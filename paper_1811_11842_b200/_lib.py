@@ -75,13 +75,15 @@ lib.ch_reset_stats.argtypes = [_P]
 lib.ch_enable_timing.argtypes = [_P, C.c_int]
 lib.ch_set_time_index.argtypes = [_P, C.c_int64]
 lib.ch_get_time_index.argtypes = [_P, C.POINTER(C.c_int64)]
+lib.ch_comm_mode.argtypes = [_P]
+lib.ch_selftest_xrank.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]
 
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = ("ch_create", "ch_comm_unique_id", "ch_comm_init", "ch_local_rows", "ch_partition", "ch_set_stream",
            "ch_set_fields", "ch_set_field", "ch_step", "ch_get_fields", "ch_get_field",
            "ch_apply_operator", "ch_solve", "ch_get_stats", "ch_reset_stats", "ch_enable_timing",
            "ch_last_error", "ch_abi_version", "ch_destroy", "ch_set_time_index",
-           "ch_get_time_index")
+           "ch_get_time_index", "ch_comm_mode", "ch_selftest_xrank")
 
 
 class CHError(RuntimeError):

@@ -12,7 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libch_b200.so")
-SOURCES = ["api.cu", "kernels_aux.cu", "kernels_ch.cu", "kernels_rhs.cu", "kernels_cgs.cu", "comm.cu"]
+SOURCES = ["api.cu", "kernels_aux.cu", "kernels_ch.cu", "kernels_rhs.cu", "kernels_cgs.cu", "comm.cu",
+           "xrank.cu"]
 NVCC = os.environ.get("NVCC", "nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]

@@ -6,6 +6,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <unistd.h>
+
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -31,6 +33,8 @@ enum Arr {
   A_N = A_ZH0 + CGM - 1
 };
 
+constexpr size_t XR_TOT_BYTES = (size_t)2 * XS_MAX * 8 * sizeof(double);
+constexpr size_t XR_BYTES = XR_TOT_BYTES + 256;   // totals + XR_MAX flags (padded)
 constexpr int MAX_BLOCKS = 1 << 20;  // reduction partials (8 doubles each): covers 16384^2 grids
 constexpr int NSC = CH_NSYS + 2;  // one KScal per system + apply + spare
 
@@ -92,6 +96,15 @@ struct ch_handle {
                               // halo rows and cross-slab finalize (env CHB_MS=0: per-slab
                               // launches + halo copies + finalize kernel)
   int64_t tidx = 0;           // time index n of the state (ch_set_time_index; R23 start-up)
+  // cross-rank / cross-slab combine of the multi-slab CG sweep (common.cuh XPeers)
+  void* xr_mem = nullptr;     // this rank's totals area [2][XS_MAX][8] + flags [XR_MAX]
+  XPeers* xp_dev = nullptr;   // device copy of the peer table
+  unsigned epoch = 0;         // multi-slab sweep launches so far (same on every rank)
+  int p2p = 0;                // ranks combine and exchange halo rows over NVLink peer memory
+  double* nb_lo[A_N] = {};    // lower / upper neighbouring rank's boundary-slab arrays,
+  double* nb_hi[A_N] = {};    // peer-mapped (ring arrays only; p2p)
+  int nb_lo_j0 = 0, nb_hi_j0 = 0;
+  std::vector<void*> ipc_open;  // peer mappings to close at ch_destroy
 };
 
 namespace {
@@ -226,6 +239,9 @@ RedArgs rargs(ch_handle* h, int fin, int sys, int slab) {
   ra.nbs = 0;
   ra.nslab = h->S;
   ra.ticket2 = h->ticket + MS_MAX;
+  ra.xp = nullptr;
+  ra.epoch = 0;
+  ra.pad2 = 0;
   return ra;
 }
 
@@ -345,6 +361,13 @@ int solve_status(ch_handle* h, int sys, const char* name) {
   h->stats.iters_last[sys] = s.iter;
   h->stats.iters_total[sys] += s.iter;
   h->stats.resid_last[sys] = s.bb > 0 ? sqrt(s.rr / s.bb) : 0.0;
+  if (s.status == KS_PEER_TIMEOUT) {
+    char buf[200];
+    snprintf(buf, sizeof buf, "%s: peer-memory combine timed out at iteration %d of step %lld "
+             "(a rank's totals never arrived)", name, s.iter, (long long)h->tidx);
+    h->err = buf;
+    return CH_ERR_COMM;
+  }
   if (s.status == 1 || s.status >= 3) {
     static const char* what[] = {
         "", "zero or non-finite inner product", "",
@@ -514,7 +537,30 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
                                     8.0 * (m + 4) * (double)(K / m)) * cells;
   } else {
   const int tt = h->cg3 && NZ >= 3;
-  const bool ms_launch = h->ms && h->S > 1 && h->S <= MS_MAX && !h->comm;
+  // one sweep launch over all local slabs with in-kernel halo rows and the
+  // peer-memory combine: virtual slabs of one process, or ranks with P2P
+  const bool ms_launch = h->ms && h->S <= MS_MAX && (h->p2p || (h->S > 1 && !h->comm));
+  // neighbour array `id` of local slab s, offset to global rows (dir -1: below)
+  auto nbp = [&](int s, int id, int dir) -> double* {
+    const Slab& sl = h->sl[s];
+    const double* base = nullptr;
+    int j0 = 0;
+    if (dir < 0 && s > 0) {
+      base = h->sl[s - 1].a[id];
+      j0 = h->sl[s - 1].g.j0;
+    } else if (dir < 0 && h->p2p) {
+      base = h->nb_lo[id];
+      j0 = h->nb_lo_j0;
+    } else if (dir > 0 && s + 1 < h->S) {
+      base = h->sl[s + 1].a[id];
+      j0 = h->sl[s + 1].g.j0;
+    } else if (dir > 0 && h->p2p) {
+      base = h->nb_hi[id];
+      j0 = h->nb_hi_j0;
+    }
+    if (!base) return nullptr;
+    return const_cast<double*>(base) + (long)(sl.g.j0 - j0) * (long)sl.g.pitch;
+  };
   long k = 0;
   int chunk = 4;
   for (;;) {
@@ -539,12 +585,19 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
           ma.so[s] = so >= 0 ? sl.a[so] : nullptr;
           ma.w[s] = od.w;
           ma.a[s] = od.a;
+          ma.zlo[s] = nbp(s, zo, -1);
+          ma.zhi[s] = nbp(s, zo, 1);
+          ma.slo[s] = so >= 0 ? nbp(s, so, -1) : nullptr;
+          ma.shi[s] = so >= 0 ? nbp(s, so, 1) : nullptr;
         }
+        ma.sysfence = h->p2p;
+        RedArgs ra = rargs(h, FIN_CGS, sys, 0);
+        ra.xp = h->xp_dev;
+        ra.epoch = ++h->epoch;
         KTime kt(h, kc_sys, cgs_bytes(ekind, first, tt) * cells, k + 1);
         h->stats.launches -= h->S - 1;   // one launch for all slabs
         h->stats.kc_launches[kc_sys] -= h->S - 1;
-        launch_cgs_iter_ms(opdesc(h, kind, h->sl[0]), ma, first, dir, tt,
-                           rargs(h, FIN_CGS, sys, 0), h->st);
+        launch_cgs_iter_ms(opdesc(h, kind, h->sl[0]), ma, first, dir, tt, ra, h->st);
       } else {
         {
           KTime kt(h, kc_sys, cgs_bytes(ekind, first, tt) * cells, k + 1);
@@ -1090,6 +1143,10 @@ static void destroy_mem(ch_handle* h) {
   if (h->cgtab) cudaFree(h->cgtab);
   if (h->pbar) cudaFree(h->pbar);
   if (h->gm_host) cudaFreeHost(h->gm_host);
+  for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
+  h->ipc_open.clear();
+  if (h->xr_mem) cudaFree(h->xr_mem);
+  if (h->xp_dev) cudaFree(h->xp_dev);
   for (auto& r : h->tm.pending) {
     cudaEventDestroy(r.e0);
     cudaEventDestroy(r.e1);
@@ -1098,6 +1155,150 @@ static void destroy_mem(ch_handle* h) {
   h->tm.pending.clear();
   h->tm.pool.clear();
 }
+
+}  // extern "C"
+
+namespace {
+
+// The arrays of the CG z ring (and s ping-pong) in a fixed order, the same on
+// every rank: the peer-mapped sweep stores its edge rows of z' into these.
+constexpr int NRING_MAX = 4 + CGM - 1;
+int ring_ids(const ch_handle* h, int* ids) {
+  int n = 0;
+  ids[n++] = A_Z;
+  ids[n++] = A_R;
+  ids[n++] = A_RH;
+  ids[n++] = A_BP;
+  for (int k = 0; k + 1 < h->cg_defer; ++k) ids[n++] = A_ZH0 + k;
+  return n;
+}
+
+struct PeerInfo {
+  int32_t pid, cg_defer, S, nring;
+  int32_t j0_first, j0_last, ok, pad;
+  char bus[16];                              // PCI bus id of the rank's device
+  cudaIpcMemHandle_t xr;                     // totals area + flags
+  cudaIpcMemHandle_t first[NRING_MAX], last[NRING_MAX];  // ring arrays, first / last slab
+};
+
+// After the NCCL clique exists: agree on the deferred-p/x block length (the
+// z ring must index the same arrays on every rank), then try to map the
+// neighbours' ring arrays and every rank's totals area through CUDA IPC
+// (NVLink peer memory).  P2P is used only if every rank is a separate process
+// on its own device with peer access to all the others (never two ranks on
+// one GPU: their sweeps wait on one another) and CHB_P2P is not 0; otherwise
+// the per-iteration NCCL group stays in use.
+int peer_setup(ch_handle* h) {
+  const int R = h->grid.nranks, me = h->grid.rank, S = h->S;
+  PeerInfo mine;
+  memset(&mine, 0, sizeof mine);
+  mine.pid = (int32_t)getpid();
+  mine.cg_defer = h->cg_defer;
+  mine.S = S;
+  int ids[NRING_MAX];
+  mine.nring = ring_ids(h, ids);
+  mine.j0_first = h->sl.front().g.j0;
+  mine.j0_last = h->sl.back().g.j0;
+  int ok = 1;
+  if (const char* e = getenv("CHB_P2P")) ok = atoi(e) != 0;
+  if (R > XR_MAX || R * S > XS_MAX || S > MS_MAX || !h->ms) ok = 0;
+  if (cudaDeviceGetPCIBusId(mine.bus, sizeof mine.bus, h->grid.device) != cudaSuccess) ok = 0;
+  if (ok && cudaIpcGetMemHandle(&mine.xr, h->xr_mem) != cudaSuccess) ok = 0;
+  for (int i = 0; ok && i < mine.nring; ++i)
+    if (cudaIpcGetMemHandle(&mine.first[i], h->sl.front().a[ids[i]]) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine.last[i], h->sl.back().a[ids[i]]) != cudaSuccess)
+      ok = 0;
+  cudaGetLastError();  // an IPC refusal is not a CUDA error of the step
+  std::vector<PeerInfo> all(R);
+  if (comm_allgather_host(h->comm, &mine, all.data(), sizeof(PeerInfo), h->st) != 0) {
+    h->err = "peer setup: allgather failed";
+    return CH_ERR_COMM;
+  }
+  for (const PeerInfo& q : all) h->cg_defer = std::min(h->cg_defer, (int)q.cg_defer);
+  // local verdict: distinct processes on distinct devices with peer access
+  for (int q = 0; q < R && ok; ++q) {
+    if (q == me) continue;
+    int dq = -1, can = 0;
+    if (all[q].pid == mine.pid) ok = 0;
+    if (ok && cudaDeviceGetByPCIBusId(&dq, all[q].bus) != cudaSuccess) ok = 0;
+    if (ok && dq == h->grid.device) ok = 0;
+    if (ok && (cudaDeviceCanAccessPeer(&can, h->grid.device, dq) != cudaSuccess || !can)) ok = 0;
+  }
+  cudaGetLastError();
+  auto agree = [&](int v, int* all_ok) -> int {
+    std::vector<int32_t> flags(R);
+    int32_t x = v;
+    if (comm_allgather_host(h->comm, &x, flags.data(), sizeof x, h->st) != 0) return CH_ERR_COMM;
+    *all_ok = 1;
+    for (int32_t f : flags) *all_ok &= f != 0;
+    return CH_OK;
+  };
+  int all_ok = 0;
+  if (agree(ok && mine.pid != 0, &all_ok) != CH_OK) {
+    h->err = "peer setup: allgather failed";
+    return CH_ERR_COMM;
+  }
+  if (!all_ok) return CH_OK;  // NCCL halos and allgather per iteration
+  // map: every rank's totals area, the neighbours' boundary-slab ring arrays
+  XPeers xp;
+  memset(&xp, 0, sizeof xp);
+  xp.R = R;
+  xp.rank = me;
+  xp.slab0 = me * S;
+  xp.nslab_all = R * S;
+  auto open = [&](const cudaIpcMemHandle_t& hd) -> void* {
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    h->ipc_open.push_back(p);
+    return p;
+  };
+  int mapped = 1;
+  for (int q = 0; q < R && mapped; ++q) {
+    char* base = q == me ? static_cast<char*>(h->xr_mem) : static_cast<char*>(open(all[q].xr));
+    if (!base) {
+      mapped = 0;
+      break;
+    }
+    xp.tot[q] = reinterpret_cast<double*>(base);
+    xp.flag[q] = reinterpret_cast<unsigned*>(base + XR_TOT_BYTES);
+  }
+  const int nr = ring_ids(h, ids);  // the agreed block length
+  for (int i = 0; i < nr && mapped; ++i) {
+    if (me > 0) {
+      h->nb_lo[ids[i]] = static_cast<double*>(open(all[me - 1].last[i]));
+      mapped &= h->nb_lo[ids[i]] != nullptr;
+    }
+    if (me + 1 < R) {
+      h->nb_hi[ids[i]] = static_cast<double*>(open(all[me + 1].first[i]));
+      mapped &= h->nb_hi[ids[i]] != nullptr;
+    }
+  }
+  if (me > 0) h->nb_lo_j0 = all[me - 1].j0_last;
+  if (me + 1 < R) h->nb_hi_j0 = all[me + 1].j0_first;
+  CK(cudaMemsetAsync(h->xr_mem, 0, XR_BYTES, h->st));
+  h->epoch = 0;
+  if (agree(mapped, &all_ok) != CH_OK) {
+    h->err = "peer setup: allgather failed";
+    return CH_ERR_COMM;
+  }
+  if (!all_ok) {
+    for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
+    h->ipc_open.clear();
+    for (int i = 0; i < A_N; ++i) h->nb_lo[i] = h->nb_hi[i] = nullptr;
+    cudaGetLastError();
+    return CH_OK;
+  }
+  CK(cudaMemcpy(h->xp_dev, &xp, sizeof xp, cudaMemcpyHostToDevice));
+  h->p2p = 1;
+  return CH_OK;
+}
+
+}  // namespace
+
+extern "C" {
 
 ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) {
   auto fail = [&](int code, ch_handle* h, const char* msg) -> ch_handle* {
@@ -1201,6 +1402,21 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
       cudaMalloc(&h->gm_red, (size_t)(S + 1) * 72 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->gm_host, (size_t)std::max(192, 72 * S) * sizeof(double)) != cudaSuccess)
     return fail(CH_ERR_CUDA, h, "cudaMalloc (scalars)");
+  if (cudaMalloc(&h->xr_mem, XR_BYTES) != cudaSuccess ||
+      cudaMalloc(&h->xp_dev, sizeof(XPeers)) != cudaSuccess)
+    return fail(CH_ERR_CUDA, h, "cudaMalloc (peer table)");
+  cudaMemset(h->xr_mem, 0, XR_BYTES);
+  {
+    XPeers xp;
+    memset(&xp, 0, sizeof xp);
+    xp.R = 1;
+    xp.rank = 0;
+    xp.slab0 = 0;
+    xp.nslab_all = S;
+    xp.tot[0] = static_cast<double*>(h->xr_mem);
+    xp.flag[0] = reinterpret_cast<unsigned*>(static_cast<char*>(h->xr_mem) + XR_TOT_BYTES);
+    cudaMemcpy(h->xp_dev, &xp, sizeof xp, cudaMemcpyHostToDevice);
+  }
   cudaMemset(h->sc, 0, NSC * sizeof(KScal));
   memset(h->sch, 0, NSC * sizeof(KScal));
   cudaMemset(h->ticket, 0, (MS_MAX + 1) * sizeof(unsigned int));
@@ -1222,7 +1438,13 @@ int ch_comm_init(ch_handle* h, const void* id, size_t len) {
   if (!h) return CH_ERR_ARG;
   if (h->grid.nranks == 1) return CH_OK;
   h->comm = comm_create(id, len, h->grid.rank, h->grid.nranks, h->grid.device, &h->err);
-  return h->comm ? CH_OK : CH_ERR_COMM;
+  if (!h->comm) return CH_ERR_COMM;
+  return peer_setup(h);
+}
+
+int ch_comm_mode(const ch_handle* h) {
+  if (!h) return -CH_ERR_ARG;
+  return !h->comm ? 0 : (h->p2p ? 2 : 1);
 }
 
 int ch_local_rows(const ch_handle* h, int32_t* row0, int32_t* nrows) {

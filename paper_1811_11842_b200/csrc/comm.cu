@@ -149,6 +149,18 @@ int comm_allreduce_sum(Comm* c, const double* send, double* recv, size_t count, 
                                                                                               : 1;
 }
 
+int comm_allgather_host(Comm* c, const void* send, void* recv, size_t bytes, cudaStream_t st) {
+  char* d = nullptr;
+  const size_t n = (size_t)c->nranks * bytes;
+  if (cudaMalloc(&d, n + bytes) != cudaSuccess) return 1;
+  int bad = cudaMemcpyAsync(d + n, send, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess;
+  if (!bad) bad = api().AllGather(d + n, d, bytes, ncclUint8, c->comm, st) != ncclSuccess;
+  if (!bad) bad = cudaMemcpyAsync(recv, d, n, cudaMemcpyDeviceToHost, st) != cudaSuccess;
+  if (!bad) bad = cudaStreamSynchronize(st) != cudaSuccess;
+  cudaFree(d);
+  return bad;
+}
+
 void comm_destroy(Comm* c) {
   if (!c) return;
   api().CommDestroy(c->comm);

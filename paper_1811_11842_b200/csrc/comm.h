@@ -31,4 +31,7 @@ int comm_iter_exchange(Comm* c, const double* send, double* recv, size_t count,
                        const HaloSpec* halos, int nhalo, int pitch, cudaStream_t st);
 // recv = sum over ranks of send (`count` device doubles, distinct buffers), on stream st (0 = ok)
 int comm_allreduce_sum(Comm* c, const double* send, double* recv, size_t count, cudaStream_t st);
+// recv[r * bytes .. (r+1) * bytes) = send of rank r; host buffers (staged
+// through device memory, synchronous on st): setup-time metadata only
+int comm_allgather_host(Comm* c, const void* send, void* recv, size_t bytes, cudaStream_t st);
 void comm_destroy(Comm* c);

@@ -192,7 +192,8 @@ enum KStatus : int {
   KS_BI_RHO = 7,     // BiCGStab (r^, r) = 0 or not finite
   KS_BI_RV = 8,      // BiCGStab (r^, v) = 0 or not finite
   KS_BI_TT = 9,      // BiCGStab (t, t) = 0 or not finite, or omega = 0
-  KS_RES_NAN = 10    // residual norm not finite
+  KS_RES_NAN = 10,   // residual norm not finite
+  KS_PEER_TIMEOUT = 11  // cross-rank combine: a rank's totals never arrived (~2 s)
 };
 __device__ __forceinline__ void kfail(KScal* s, int code, double val) {
   s->status = code;
@@ -498,6 +499,23 @@ __device__ __forceinline__ void trace_pt(int i) {
 // finish (atomic ticket) sums the partials in fixed block order (deterministic)
 // and either finalizes inline (single slab, single rank) or stores the slab
 // total for a later cross-slab finalize.
+// Cross-rank combine of the per-slab totals of one CG iteration over peer
+// memory (NVLink P2P between the processes of a clique; within one process
+// the same code with R = 1).  Every rank owns a totals area [2][XS_MAX][8]
+// (double-buffered by iteration parity) and XR_MAX arrival flags; the last
+// slab of a rank to finish pushes its slabs' totals into EVERY rank's area
+// (peer stores), then stores the iteration's epoch into its flag on every
+// rank (release, system scope), waits until all R flags on its own rank
+// carry the epoch (acquire) and sums the totals in global slab order: every
+// rank computes bit-identical scalars with no NCCL call and no extra launch.
+constexpr int XR_MAX = 8, XS_MAX = 64;
+struct XPeers {
+  int R, rank;            // ranks in the clique, this rank
+  int slab0, nslab_all;   // global index of this rank's first slab; slabs over all ranks
+  double* tot[XR_MAX];    // rank q's totals area (peer-mapped; [rank] is local)
+  unsigned* flag[XR_MAX]; // rank q's arrival flags [XR_MAX] (peer-mapped)
+};
+
 struct RedArgs {
   double* part;          // [nblocks * 8]
   unsigned int* ticket;  // zeroed; reset by the last block (multi-slab launch: one per slab)
@@ -514,7 +532,71 @@ struct RedArgs {
   int nbs;
   int nslab;
   unsigned int* ticket2;
+  // multi-slab launch: cross-rank combine (xp: device XPeers; epoch: this
+  // launch's number, > 0, the same on every rank)
+  const XPeers* xp;
+  unsigned epoch;
+  int pad2;
 };
+
+// The combine of one rank's last slab (one warp, all lanes): push the nloc
+// local slab totals (loc[s * 8 + k]) to every rank, arrive, wait for every
+// rank, sum the totals of all slabs in slab order into t.  false: a rank did
+// not arrive within ~2 s (the caller reports KS_PEER_TIMEOUT; never a hang).
+template <int K>
+__device__ __forceinline__ bool xrank_combine(const XPeers* xpp, unsigned epoch, const double* loc,
+                                              int nloc, double (&t)[8]) {
+  const int lane = threadIdx.x & 31;
+  const int R = xpp->R, me = xpp->rank, slab0 = xpp->slab0, nall = xpp->nslab_all;
+  const size_t par = (size_t)(epoch & 1u) * XS_MAX;
+  const int n = R * nloc * K;
+  for (int i = lane; i < n; i += 32) {
+    const int q = i / (nloc * K), r = i % (nloc * K), sl = r / K, k = r % K;
+    const double v = __ldcg(loc + sl * 8 + k);
+    double* dst = xpp->tot[q] + (par + slab0 + sl) * 8 + k;
+    asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(dst), "d"(v) : "memory");
+  }
+  // every lane's pushes are ordered before the flags (system scope)
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  __syncwarp();
+  if (lane < R) {
+    unsigned* f = xpp->flag[lane] + me;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+  }
+  // every lane acquires every rank's flag on this rank (so each lane's loads
+  // below see every rank's pushes)
+  const unsigned* myf = xpp->flag[me];
+  int ok = 1;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int q = 0; q < R && ok; ++q) {
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(myf + q) : "memory");
+      if (v == epoch) break;
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > 2000000000ull) {   // 2 s
+        ok = 0;
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  if (!__all_sync(0xffffffffu, ok)) return false;
+  const double* mine = xpp->tot[me] + par * 8;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double a = 0.0;
+    for (int sl = 0; sl < nall; ++sl) {
+      double v;
+      asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(mine + sl * 8 + k) : "memory");
+      a += v;   // global slab order: identical on every rank
+    }
+    t[k] = a;
+  }
+  return true;
+}
 
 template <int K>
 __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedArgs& ra,
@@ -617,14 +699,22 @@ __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedA
     }
     prev = __shfl_sync(FULL, prev, 0);
     if (prev != (unsigned)(ra.nslab - 1)) return;
-    double t[8];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double a = 0.0;
-      for (int s = 0; s < ra.nslab; ++s) a += __ldcg(ra.tot + s * 8 + k);   // slab order
-      t[k] = a;
-    }
     if (lane == 0) *ra.ticket2 = 0u;
+    double t[8];
+    if (ra.xp) {
+      // across ranks (and the slabs of this one): peer-memory combine
+      if (!xrank_combine<K>(ra.xp, ra.epoch, ra.tot, ra.nslab, t)) {
+        if (lane == 0) kfail(ra.sc, KS_PEER_TIMEOUT, (double)ra.epoch);
+        return;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double a = 0.0;
+        for (int s = 0; s < ra.nslab; ++s) a += __ldcg(ra.tot + s * 8 + k);   // slab order
+        t[k] = a;
+      }
+    }
     finalize_warp(ra.fin, t, ra.sc, ra.fc);
   } else if (lane == 0) {
 #pragma unroll
@@ -640,6 +730,15 @@ constexpr int MS_MAX = 8;
 struct MsArgs {
   int S;     // slabs in the launch (0 or 1: single-slab launch)
   int nbs;   // blocks per slab
+  int sysfence;  // the edge rows go to another GPU (peer pointers): fence at system scope
+  int pad;
+  // neighbour arrays of slab s pre-offset so that [off(g[s], gq, c)] addresses
+  // global row gq there (slab s-1 / s+1 of this process, or the neighbouring
+  // rank's boundary slab through peer memory); nullptr at the domain walls
+  double* zlo[MS_MAX];
+  double* zhi[MS_MAX];
+  double* slo[MS_MAX];
+  double* shi[MS_MAX];
   Geom g[MS_MAX];
   const double* zi[MS_MAX];
   double* zo[MS_MAX];

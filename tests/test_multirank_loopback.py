@@ -39,7 +39,7 @@ def _run_ranks(nx, ny, nranks, steps, vslabs=1, **kw):
     from paper_1811_11842_b200 import Simulation, unique_id
     from workloads import initial_fields
     uid = unique_id()
-    out, its, errs = [None] * nranks, [None] * nranks, []
+    out, its, errs, modes = [None] * nranks, [None] * nranks, [], [None] * nranks
     sims = [Simulation(nx, ny, rank=r, nranks=nranks, device=0, virtual_slabs=vslabs, **kw)
             for r in range(nranks)]
 
@@ -48,6 +48,7 @@ def _run_ranks(nx, ny, nranks, steps, vslabs=1, **kw):
             sim = sims[r]
             sim.set_stream(torch.cuda.Stream())
             sim.comm_init(uid)
+            modes[r] = sim.comm_mode
             rows = (sim.row0, sim.row0 + sim.nrows)
             sim.set_fields(**initial_fields(nx, ny, seed=4, rows=rows))
             sim.step(steps)
@@ -65,6 +66,9 @@ def _run_ranks(nx, ny, nranks, steps, vslabs=1, **kw):
     for s in sims:
         s.close()
     assert not errs, errs
+    # ranks sharing one GPU never use the peer-memory sweep (their kernels
+    # would wait on one another): the NCCL transport carries the iteration
+    assert modes == ["nccl"] * nranks, modes
     glob = {k: np.zeros((ny, nx)) for k in FIELDS}
     for (r0, r1), f in out:
         for k in FIELDS:
