@@ -277,9 +277,12 @@ def run_ours(args, rank, world, local_rank):
                 "config": {"workload": cfg["name"] if args.steps == cfg["steps"] else
                            f"{nx}x{ny}_{args.steps}steps (declared: {cfg['steps']})",
                            "nx": nx, "ny": ny, "dt": cfg["dt"],
-                           "parallelism": f"slab-y x{world}", "ch_solver": args.ch_solver,
+                           "parallelism": f"slab-y x{world}", "transport": sim.comm_mode,
+                           "ch_solver": args.ch_solver,
                            "rtol": sp.rtol, "true_residual_refine": sp.refine,
-                           "l2": "inputs larger than L2 (134 MB per field)",
+                           "l2": (f"inputs larger than L2 ({nx * ny * 8 / 1e6:.0f} MB per field)"
+                                  if nx * ny * 8 > 126e6 else
+                                  f"inputs fit in L2 ({nx * ny * 8 / 1e6:.1f} MB per field)"),
                            "krylov_iters_per_step": iters_step},
                 "cell_steps_per_s": value * nx * ny,
                 "roofline": roof, "kernels": per_class, "cpu_baseline": cpu, "e2e": e2e,

@@ -485,6 +485,17 @@ __device__ __forceinline__ void trace_smid() {
   asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
   chb_trace_smid[blockIdx.x] = sm;
 }
+// dispatch order of the CTA on its SM: a per-SM counter taken at entry (the
+// raw count; every launch adds its resident CTAs per SM, so count mod per-SM
+// residency is the order within the launch)
+__device__ unsigned int chb_trace_smctr[1024];
+__device__ unsigned int chb_trace_order[8192];
+__device__ __forceinline__ void trace_order() {
+  if (threadIdx.x != 0) return;
+  unsigned int sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  chb_trace_order[blockIdx.x] = atomicAdd(&chb_trace_smctr[sm & 1023], 1u);
+}
 __device__ __forceinline__ void trace_pt(int i) {
   unsigned long long gt, ck;
   trace_now(gt, ck);
@@ -600,13 +611,16 @@ __device__ __forceinline__ bool xrank_combine(const XPeers* xpp, unsigned epoch,
 
 template <int K>
 __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedArgs& ra,
-                                                      const CgsPre* pre = nullptr) {
+                                                      const CgsPre* pre = nullptr,
+                                                      int bid_override = -1) {
   __shared__ double sm[32][K > 0 ? K : 1];
   __shared__ int am_last;
   const int tid = threadIdx.x + threadIdx.y * blockDim.x;
   const int lane = tid & 31, wid = tid >> 5;
   const int nw = (blockDim.x * blockDim.y + 31) >> 5;
-  const int gbid = blockIdx.x + blockIdx.y * gridDim.x;
+  // bid_override: the CTA's claimed tile (partials indexed by tile: the
+  // fixed-order sum stays deterministic whichever CTA took which tile)
+  const int gbid = bid_override >= 0 ? bid_override : (int)(blockIdx.x + blockIdx.y * gridDim.x);
   const int ms_slab = ra.nbs > 0 ? gbid / ra.nbs : ra.slab;
   const int bid = ra.nbs > 0 ? gbid % ra.nbs : gbid;
   const int nb = ra.nbs > 0 ? ra.nbs : gridDim.x * gridDim.y;

@@ -43,6 +43,7 @@ assert rc == 0, rc
 raw = np.fromfile(path, dtype=np.uint8)
 t = raw[: a.nb * 128].view(np.uint64).reshape(a.nb, 16).astype(np.int64)
 smid = raw[a.nb * 128: a.nb * 132].view(np.uint32)
+order_raw = raw[a.nb * 132: a.nb * 136].view(np.uint32) if raw.size >= a.nb * 136 else None
 gt, ck = t[:, :8], t[:, 8:]
 base = gt[:, 0].min()
 rel = (gt - base) / 1e3  # us
@@ -67,4 +68,13 @@ out["per_sm"] = {"n_sm": len(per_sm), "ctas_per_sm": sorted({len(v) for v in per
                  "std_across_sm_means": round(float(sm_mean.std()), 2),
                  "mean_std_within_sm": round(float(within), 2),
                  "sm_means_by_smid": {str(k): round(float(np.mean(v)), 2) for k, v in sorted(per_sm.items())}}
+if order_raw is not None:
+    # row-loop end time and loop duration by dispatch order on the SM
+    per = max(1, a.nb // max(1, len(per_sm)))
+    order = (order_raw % per).astype(int)
+    out["by_order"] = {str(o): {"n": int((order == o).sum()),
+                                "loop_us_mean": round(float(loop[order == o].mean()), 2),
+                                "loop_end_us_mean": round(float(rel[order == o, 3].mean()), 2),
+                                "loop_end_us_max": round(float(rel[order == o, 3].max()), 2)}
+                       for o in range(per) if (order == o).any()}
 print(json.dumps(out))
