@@ -73,8 +73,11 @@ __device__ __forceinline__ void rm_tile(int b, int nb, int ncb, int nyl, int& ch
 }
 }  // namespace
 
+#ifndef CHB_MINB_CH
+#define CHB_MINB_CH 1   // resident CTAs per SM requested from ptxas (build knob)
+#endif
 template <int NDOT, int PRE>
-__global__ void __launch_bounds__(RM_T) k_ch_rm(Geom g, ChCoef cc, const double* __restrict__ x,
+__global__ void __launch_bounds__(RM_T, CHB_MINB_CH) k_ch_rm(Geom g, ChCoef cc, const double* __restrict__ x,
                                                 double* __restrict__ y,
                                                 const double* __restrict__ d1,
                                                 const double* __restrict__ d2, int skip_done,

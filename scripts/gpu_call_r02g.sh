@@ -12,3 +12,7 @@ for a in 0 0.03 0.06 0.1 -0.05 0 0.06; do for op in mom_v poisson; do
   CHB_SKEWA=$a timeout 300 python scripts/kbench.py --solve $op --stride 1 >> gpurun_out/kb_skew.jsonl 2>&1
 done; done; echo kb=$? >> $S
 CHB_SKEWA=0.06 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -q -x -k "not 25_steps and not 50_steps" > gpurun_out/t_skew.log 2>&1; echo t_skew=$? >> $S
+# CH apply with 4 CTAs/SM (<= 128 registers) vs the default 3
+for v in "" _ch4; do
+  CHB_LIB=$PWD/paper_1811_11842_b200/libch_b200$v.so timeout 300 python scripts/matvec_sweep.py --sizes 4096 16384 > gpurun_out/mv$v.jsonl 2>&1
+done; echo mv=$? >> $S
