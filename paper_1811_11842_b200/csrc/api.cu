@@ -92,9 +92,6 @@ struct ch_handle {
   int cg3 = 1;                // single-reduction CG: three-term z recurrence (env CHB_CG3)
   int strip2 = 0;             // rows per strip, 0 = one resident wave (env CHB_STRIP)
   int pdl = 1;                // programmatic dependent launch of the CG sweeps (env CHB_PDL)
-  double skew = 0.0;          // CG sweep tiles claimed in arrival order with skewed strip
-                              // heights (env CHB_SKEWA; experiment, 0 = off)
-  unsigned* claims = nullptr; // device [NSC][2] claim counters
   int ms = 1;                 // virtual slabs: one sweep launch over all slabs with in-kernel
                               // halo rows and cross-slab finalize (env CHB_MS=0: per-slab
                               // launches + halo copies + finalize kernel)
@@ -418,8 +415,6 @@ OpDesc opdesc(ch_handle* h, int kind, const Slab& s) {
   d.s = 1.0;
   d.kscale = 1.0;
   d.ascal = 0.0;
-  d.skew = 0.0;
-  d.claim = nullptr;
   d.rho_n = h->prm.rho_n;
   d.rho_s = h->prm.rho_s;
   switch (kind) {
@@ -566,10 +561,6 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
     if (!base) return nullptr;
     return const_cast<double*>(base) + (long)(sl.g.j0 - j0) * (long)sl.g.pitch;
   };
-  // claimed skewed tiles (experiment): single slab, one resident wave, tall strips
-  const bool skew_on = h->skew != 0.0 && h->S == 1 && h->strip2 == 0 && !ms_launch &&
-                       h->sl[0].g.nyl >= 64;
-  if (skew_on) CK(cudaMemsetAsync(h->claims + 2 * sys, 0, 2 * sizeof(unsigned), h->st));
   long k = 0;
   int chunk = 4;
   for (;;) {
@@ -612,15 +603,9 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
           KTime kt(h, kc_sys, cgs_bytes(ekind, first, tt) * cells, k + 1);
           for (int s = 0; s < h->S; ++s) {
             Slab& sl = h->sl[s];
-            OpDesc od = opdesc(h, kind, sl);
-            RedArgs ra = rargs(h, FIN_CGS, sys, s);
-            if (skew_on) {
-              od.skew = h->skew;
-              od.claim = h->claims + 2 * sys;
-              ra.epoch = (unsigned)k;   // claim counter parity
-            }
-            launch_cgs_iter(od, sl.g, sl.a[zi], sl.a[zo], sl.a[si], so >= 0 ? sl.a[so] : nullptr,
-                            first, dir, tt, ra, h->st);
+            launch_cgs_iter(opdesc(h, kind, sl), sl.g, sl.a[zi], sl.a[zo], sl.a[si],
+                            so >= 0 ? sl.a[so] : nullptr, first, dir, tt,
+                            rargs(h, FIN_CGS, sys, s), h->st);
           }
         }
         TRY(iter_exchange(h, FIN_CGS, sys, 3, zo, so));
@@ -1161,7 +1146,6 @@ static void destroy_mem(ch_handle* h) {
   for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
   h->ipc_open.clear();
   if (h->xr_mem) cudaFree(h->xr_mem);
-  if (h->claims) cudaFree(h->claims);
   if (h->xp_dev) cudaFree(h->xp_dev);
   for (auto& r : h->tm.pending) {
     cudaEventDestroy(r.e0);
@@ -1353,7 +1337,6 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   if (const char* e = getenv("CHB_STRIP")) h->strip2 = std::max(0, atoi(e));
   if (const char* e = getenv("CHB_PDL")) h->pdl = atoi(e) != 0;
   if (const char* e = getenv("CHB_MS")) h->ms = atoi(e) != 0;
-  if (const char* e = getenv("CHB_SKEWA")) h->skew = atof(e);
   if (const char* e = getenv("CHB_DEFER")) h->cg_defer = std::min(std::max(2, atoi(e)), CGM);
   if (const char* e = getenv("CHB_PERSIST")) h->persist = atoi(e) != 0;
   memset(&h->stats, 0, sizeof(ch_stats));
@@ -1420,9 +1403,7 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
       cudaMalloc(&h->gm_red, (size_t)(S + 1) * 72 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->gm_host, (size_t)std::max(192, 72 * S) * sizeof(double)) != cudaSuccess)
     return fail(CH_ERR_CUDA, h, "cudaMalloc (scalars)");
-  if (cudaMalloc(&h->claims, NSC * 2 * sizeof(unsigned)) != cudaSuccess ||
-      cudaMemset(h->claims, 0, NSC * 2 * sizeof(unsigned)) != cudaSuccess ||
-      cudaMalloc(&h->xr_mem, XR_BYTES) != cudaSuccess ||
+  if (cudaMalloc(&h->xr_mem, XR_BYTES) != cudaSuccess ||
       cudaMalloc(&h->xp_dev, sizeof(XPeers)) != cudaSuccess)
     return fail(CH_ERR_CUDA, h, "cudaMalloc (peer table)");
   cudaMemset(h->xr_mem, 0, XR_BYTES);

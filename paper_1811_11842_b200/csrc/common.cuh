@@ -611,16 +611,13 @@ __device__ __forceinline__ bool xrank_combine(const XPeers* xpp, unsigned epoch,
 
 template <int K>
 __device__ __forceinline__ void block_reduce_finalize(double (&v)[K], const RedArgs& ra,
-                                                      const CgsPre* pre = nullptr,
-                                                      int bid_override = -1) {
+                                                      const CgsPre* pre = nullptr) {
   __shared__ double sm[32][K > 0 ? K : 1];
   __shared__ int am_last;
   const int tid = threadIdx.x + threadIdx.y * blockDim.x;
   const int lane = tid & 31, wid = tid >> 5;
   const int nw = (blockDim.x * blockDim.y + 31) >> 5;
-  // bid_override: the CTA's claimed tile (partials indexed by tile: the
-  // fixed-order sum stays deterministic whichever CTA took which tile)
-  const int gbid = bid_override >= 0 ? bid_override : (int)(blockIdx.x + blockIdx.y * gridDim.x);
+  const int gbid = blockIdx.x + blockIdx.y * gridDim.x;
   const int ms_slab = ra.nbs > 0 ? gbid / ra.nbs : ra.slab;
   const int bid = ra.nbs > 0 ? gbid % ra.nbs : gbid;
   const int nb = ra.nbs > 0 ? ra.nbs : gridDim.x * gridDim.y;

@@ -287,8 +287,6 @@ static Op5T make_op(const OpDesc& d) {
   o.rho_n = d.rho_n;
   o.rho_s = d.rho_s;
   o.ascal = d.ascal;
-  o.skew = 0.0;
-  o.claim = nullptr;
   return o;
 }
 

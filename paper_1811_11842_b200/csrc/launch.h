@@ -26,8 +26,6 @@ struct OpDesc {
   const double* w;    // cell coefficient (NUTRIENT: phi_s^{1/2}; POISSON_VAR: phi^{n+1})
   double s, kscale, rho_n, rho_s;
   double ascal;       // the diagonal coefficient of the *_C kinds
-  double skew;        // CG sweep tile claiming with skewed strip heights (0 = off)
-  unsigned* claim;    // two claim counters of this system (parity of the sweep index)
 };
 
 void launch_cg5_init(const OpDesc& d, const Geom& g, const double* x, const double* b,

@@ -12,11 +12,6 @@ struct Op5T {
   const double* w;
   double s, kscale, rho_n, rho_s;
   double ascal;   // AM == 2: constant diagonal coefficient (no array)
-  // CG sweep tile claiming (experiment, env CHB_SKEWA): CTAs take tiles in
-  // arrival order from claim[parity]; within a column chunk earlier strips
-  // get (1 + skew (1 - 2k/(K-1))) times the mean height.  skew = 0: off.
-  double skew;
-  unsigned* claim;
 };
 
 // diagonal coefficient at flat offset o: AM = 0 none, 1 array a[], 2 scalar
