@@ -81,8 +81,6 @@ struct ch_handle {
   Comm* comm = nullptr;
   size_t arr_elems = 0;
   double* cgtab = nullptr;    // deferred-p/x CG coefficient tables, device [NSC][2][CGT]
-  unsigned int* pbar = nullptr; // persistent-CG grid barrier: count, generation, abort flag
-  int persist = 0;            // single-slab CG solves as one cooperative launch (env CHB_PERSIST)
   int cur_m = 0;              // block length of the solve in flight (0: cg_defer)
   int cg_defer = 64;          // block length m (2..64) of the deferred p/x CG (env CHB_DEFER);
                               // reduced at ch_create if the z history would not fit
@@ -495,47 +493,6 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   const int kc_sys = sys == CH_SYS_U ? CH_KC_CG_FUSED_U
                    : sys == CH_SYS_V ? CH_KC_CG_FUSED_V
                    : sys == CH_SYS_P ? CH_KC_CG_FUSED_P : CH_KC_CG_FUSED;
-  if (h->persist && h->S == 1 && !h->comm) {
-    // the whole solve in one cooperative launch (single slab only)
-    Slab& sl = h->sl[0];
-    PArgs pa;
-    memset(&pa, 0, sizeof pa);
-    for (int j = 0; j < NZ; ++j) pa.z[j] = sl.a[Zr[j]];
-    pa.nz = NZ;
-    pa.s[0] = sl.a[S[0]];
-    pa.s[1] = sl.a[S[1]];
-    pa.P = sl.a[P];
-    pa.X = sl.a[xid];
-    pa.sc = h->sc + sys;
-    pa.part = h->part;
-    pa.count = h->pbar;
-    pa.gen = h->pbar + 1;
-    pa.abort = reinterpret_cast<int*>(h->pbar + 2);
-    pa.fc = rargs(h, FIN_CGS, sys, 0).fc;
-    pa.m = m;
-    CK(cudaMemsetAsync(h->pbar, 0, 4 * sizeof(unsigned int), h->st));
-    {
-      KTime kt(h, kc_sys, 0.0, 1);
-      const int e = launch_cgs_persist(opdesc(h, kind, sl), sl.g, pa, h->st);
-      if (e != 0) {
-        h->err = std::string("persistent CG launch: ") + cudaGetErrorString((cudaError_t)e);
-        return CH_ERR_CUDA;
-      }
-    }
-    TRY(check_launch(h, "cgs persistent"));
-    unsigned int flags[4];
-    CK(cudaMemcpyAsync(flags, h->pbar, sizeof flags, cudaMemcpyDeviceToHost, h->st));
-    TRY(poll(h, sys));
-    if (flags[2]) {
-      h->err = "persistent CG: grid barrier timed out";
-      return CH_ERR_CUDA;
-    }
-    // algorithmic bytes of the launch: K sweeps + the in-kernel p/x updates
-    const long K = h->sch[sys].iter;
-    if (!h->tm.pending.empty() && h->tm.pending.back().kc == kc_sys)
-      h->tm.pending.back().bytes = (cgs_bytes(ekind, 0, 1) * (double)K +
-                                    8.0 * (m + 4) * (double)(K / m)) * cells;
-  } else {
   const int tt = h->cg3 && NZ >= 3;
   // one sweep launch over all local slabs with in-kernel halo rows and the
   // peer-memory combine: virtual slabs of one process, or ranks with P2P
@@ -616,7 +573,6 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
     TRY(poll(h, sys));
     if (h->sch[sys].done) break;
     if (chunk < 64) chunk *= 2;
-  }
   }
   const long K = h->sch[sys].iter;
   if (K > 0 && K % m != 0) TRY(px(K - 1, (int)(K % m), 0));
@@ -1141,7 +1097,6 @@ static void destroy_mem(ch_handle* h) {
   if (h->gm_dev) cudaFree(h->gm_dev);
   if (h->gm_red) cudaFree(h->gm_red);
   if (h->cgtab) cudaFree(h->cgtab);
-  if (h->pbar) cudaFree(h->pbar);
   if (h->gm_host) cudaFreeHost(h->gm_host);
   for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
   h->ipc_open.clear();
@@ -1338,7 +1293,6 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   if (const char* e = getenv("CHB_PDL")) h->pdl = atoi(e) != 0;
   if (const char* e = getenv("CHB_MS")) h->ms = atoi(e) != 0;
   if (const char* e = getenv("CHB_DEFER")) h->cg_defer = std::min(std::max(2, atoi(e)), CGM);
-  if (const char* e = getenv("CHB_PERSIST")) h->persist = atoi(e) != 0;
   memset(&h->stats, 0, sizeof(ch_stats));
   // rows: balanced split of ny over `total` slabs (first ny % total get one more)
   const int base = G.ny / total, rem = G.ny % total;
@@ -1399,7 +1353,6 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
       cudaMalloc(&h->tot_local, (size_t)total * 8 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&h->gm_dev, 192 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&h->cgtab, (size_t)NSC * 2 * CGT * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&h->pbar, 4 * sizeof(unsigned int)) != cudaSuccess ||
       cudaMalloc(&h->gm_red, (size_t)(S + 1) * 72 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->gm_host, (size_t)std::max(192, 72 * S) * sizeof(double)) != cudaSuccess)
     return fail(CH_ERR_CUDA, h, "cudaMalloc (scalars)");

@@ -48,22 +48,7 @@ struct ZList {
 };
 void launch_cgs_px(const Geom& g, const ZList& zl, int n, int first_block, int write_p, int need,
                    const double* T, const KScal* sc, double* P, double* X, cudaStream_t st);
-struct PArgs {
-  const double* z[CGM + 1];
-  double* s[2];
-  double* P;
-  double* X;
-  KScal* sc;
-  double* part;          // [nblocks * 4]
-  unsigned int* count;   // arrivals in the current barrier
-  unsigned int* gen;     // barrier generation
-  int* abort;
-  FinCtx fc;
-  double rdint, rdwall;
-  int nz, m, ncb, cw, PF;
-};
-// whole single-slab CG solve in one cooperative launch; returns a cudaError_t
-int launch_cgs_persist(const OpDesc& d, const Geom& g, const PArgs& pa, cudaStream_t st);
+
 void launch_cgs_delta0(const OpDesc& d, const Geom& g, const double* z, const RedArgs& ra,
                        cudaStream_t st);
 double cgs_bytes(int kind, int first, int tt);
