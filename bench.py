@@ -163,6 +163,7 @@ def run_ours(args, rank, world, local_rank):
     sim = Simulation(nx, ny, sp, rank=rank, nranks=world, device=local_rank)
     if world > 1:
         sim.comm_init(share_unique_id(dist, rank))
+    transport = sim.comm_mode
     stream = torch.cuda.current_stream()
     sim.set_stream(stream)
     rows = (sim.row0, sim.row0 + sim.nrows)
@@ -287,7 +288,7 @@ def run_ours(args, rank, world, local_rank):
                 "config": {"workload": cfg["name"] if args.steps == cfg["steps"] else
                            f"{nx}x{ny}_{args.steps}steps (declared: {cfg['steps']})",
                            "nx": nx, "ny": ny, "dt": cfg["dt"],
-                           "parallelism": f"slab-y x{world}", "transport": sim.comm_mode,
+                           "parallelism": f"slab-y x{world}", "transport": transport,
                            "ch_solver": args.ch_solver,
                            "rtol": sp.rtol, "true_residual_refine": sp.refine,
                            "l2": (f"inputs larger than L2 ({nx * ny * 8 / 1e6:.0f} MB per field)"

@@ -118,6 +118,8 @@ class Simulation:
     def comm_mode(self) -> str:
         """"single" (one process), "nccl" (NCCL group per CG iteration) or
         "p2p" (peer-memory CG iterations, ch_comm_mode)."""
+        if not self._h:
+            raise CHError(_lib.CH_ERR_ARG, "simulation is closed")
         return {0: "single", 1: "nccl", 2: "p2p"}[lib.ch_comm_mode(self._h)]
 
     def set_stream(self, stream):

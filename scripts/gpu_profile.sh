@@ -12,9 +12,7 @@ fi
 B1="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --matvec 0"
 timeout 300 $B1 > gpurun_out/plain_b1.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 5000 --csv \
-    --log-file /tmp/prof/launches_head.csv $B1 > gpurun_out/ncu_l1.log 2>&1 && \
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 30000 -c 5000 --csv \
-    --log-file /tmp/prof/launches_mid.csv $B1 > gpurun_out/ncu_l2.log 2>&1; echo launches=$? >> $S
+    --log-file /tmp/prof/launches_head.csv $B1 > gpurun_out/ncu_l1.log 2>&1; echo launches=$? >> $S
 for op in mom_v poisson; do
   timeout 300 python scripts/kbench.py --solve $op > gpurun_out/plain_$op.log 2>&1 && \
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cgs_iter -s 300 -c 2 \
