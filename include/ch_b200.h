@@ -159,8 +159,10 @@ enum {
 };
 
 /* Create a handle: allocates the rank's slab state and workspace on
- * grid->device (about 41 fields of (nrows + 4) x pitch doubles at the
- * default CG block length, halved automatically if device memory is short).
+ * grid->device (28 fields + the m - 1 = 63 z-history buffers of the
+ * deferred-p/x CG, each (nrows + 4) x pitch doubles: ~12 GB at 4096^2; m is
+ * halved automatically while the history would not fit in 80 % of the free
+ * device memory).
  * Fields start zero except c = 1.  Parameters are copied (the caller keeps
  * ownership of *grid and *params).  Returns NULL on error with *status set
  * (status may be NULL): CH_ERR_ARG for an invalid grid / parameter set,
