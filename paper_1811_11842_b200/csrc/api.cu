@@ -71,6 +71,8 @@ struct ch_handle {
   bool own_stream = false;
   KScal* sc = nullptr;       // device [NSC]
   KScal* sch = nullptr;      // pinned host [NSC]
+  KScal* pollbuf = nullptr;  // pinned host [2]: pipelined CG convergence polls
+  cudaEvent_t pollev[2] = {nullptr, nullptr};
   double* part = nullptr;
   unsigned int* ticket = nullptr;
   double* tot = nullptr;     // [nslabs_total * 8]
@@ -519,6 +521,7 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
     return const_cast<double*>(base) + (long)(sl.g.j0 - j0) * (long)sl.g.pitch;
   };
   long k = 0;
+  long npoll = 0;
   int chunk = 4;
   for (;;) {
     for (int it = 0; it < chunk; ++it, ++k) {
@@ -570,10 +573,22 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
       if ((k + 1) % m == 0) TRY(px(k, m, 1));
     }
     TRY(check_launch(h, "cgs iteration"));
-    TRY(poll(h, sys));
-    if (h->sch[sys].done) break;
+    // pipelined convergence poll: this chunk's scalars go to a pinned slot
+    // behind an event while the host waits only for the PREVIOUS chunk's --
+    // the GPU always has the next chunk queued (after convergence the sweeps
+    // of the chunk in flight exit on the device flag)
+    const int slot = (int)(npoll & 1);
+    CK(cudaMemcpyAsync(h->pollbuf + slot, h->sc + sys, sizeof(KScal), cudaMemcpyDeviceToHost,
+                       h->st));
+    CK(cudaEventRecord(h->pollev[slot], h->st));
+    ++npoll;
+    if (npoll >= 2) {
+      CK(cudaEventSynchronize(h->pollev[slot ^ 1]));
+      if (h->pollbuf[slot ^ 1].done) break;
+    }
     if (chunk < 64) chunk *= 2;
   }
+  TRY(poll(h, sys));
   const long K = h->sch[sys].iter;
   if (K > 0 && K % m != 0) TRY(px(K - 1, (int)(K % m), 0));
   {
@@ -1090,6 +1105,9 @@ static void destroy_mem(ch_handle* h) {
   h->sl.clear();
   if (h->sc) cudaFree(h->sc);
   if (h->sch) cudaFreeHost(h->sch);
+  if (h->pollbuf) cudaFreeHost(h->pollbuf);
+  for (auto& e : h->pollev)
+    if (e) cudaEventDestroy(e);
   if (h->part) cudaFree(h->part);
   if (h->ticket) cudaFree(h->ticket);
   if (h->tot) cudaFree(h->tot);
@@ -1347,6 +1365,9 @@ ch_handle* ch_create(const ch_grid* grid, const ch_params* params, int* status) 
   }
   if (cudaMalloc(&h->sc, NSC * sizeof(KScal)) != cudaSuccess ||
       cudaMallocHost(&h->sch, NSC * sizeof(KScal)) != cudaSuccess ||
+      cudaMallocHost(&h->pollbuf, 2 * sizeof(KScal)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->pollev[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->pollev[1], cudaEventDisableTiming) != cudaSuccess ||
       cudaMalloc(&h->part, (size_t)MAX_BLOCKS * 8 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&h->ticket, (MS_MAX + 1) * sizeof(unsigned int)) != cudaSuccess ||
       cudaMalloc(&h->tot, (size_t)total * 8 * sizeof(double)) != cudaSuccess ||
