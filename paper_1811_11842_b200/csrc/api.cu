@@ -1266,6 +1266,56 @@ int peer_setup(ch_handle* h) {
     return CH_OK;
   }
   CK(cudaMemcpy(h->xp_dev, &xp, sizeof xp, cudaMemcpyHostToDevice));
+  // probe the mapped clique with the stores and the combine of one sweep:
+  // edge rows of A_Z into the neighbours' ghost rows, one cross-rank combine
+  // (epoch 1); a rank whose ghost rows or sums come out wrong votes NCCL
+  {
+    const Slab& f = h->sl.front();
+    const Slab& l = h->sl.back();
+    const long P = f.g.pitch;
+    double* lo = me > 0 ? h->nb_lo[A_Z] + (long)(f.g.j0 - h->nb_lo_j0) * P : nullptr;
+    double* hi = me + 1 < R ? h->nb_hi[A_Z] + (long)(l.g.j0 - h->nb_hi_j0) * P : nullptr;
+    h->epoch = 1;
+    launch_peer_probe(h->xp_dev, h->epoch, h->tot_local, S, f.g, lo, l.g, hi, h->gm_dev, h->st);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->st));
+    int ok_probe = 1;
+    double sums[3];
+    CK(cudaMemcpy(sums, h->gm_dev, sizeof sums, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 3; ++k) {
+      double want = 0.0;
+      for (int q = 0; q < R; ++q)
+        for (int sl = 0; sl < S; ++sl) want += (q + 1.0) * (k + 1.0);
+      ok_probe &= sums[k] == want;
+    }
+    std::vector<double> row((size_t)f.g.nx);
+    auto check_rows = [&](const Slab& sb, int gq0) {
+      for (int gq = gq0; gq < gq0 + 2; ++gq) {
+        const double* src = sb.a[A_Z] + (size_t)(gq - sb.g.j0 + GH) * P;
+        if (cudaMemcpy(row.data(), src, row.size() * sizeof(double), cudaMemcpyDeviceToHost) !=
+            cudaSuccess)
+          return 0;
+        for (int c = 0; c < sb.g.nx; ++c)
+          if (row[c] != gq * 1e6 + c + 0.25) return 0;
+      }
+      return 1;
+    };
+    if (me > 0) ok_probe &= check_rows(f, f.g.j0 - 2);
+    if (me + 1 < R) ok_probe &= check_rows(l, l.g.j0 + l.g.nyl);
+    if (agree(ok_probe, &all_ok) != CH_OK) {
+      h->err = "peer setup: allgather failed";
+      return CH_ERR_COMM;
+    }
+    for (auto& sb : h->sl) CK(cudaMemsetAsync(sb.a[A_Z], 0, h->arr_elems * sizeof(double), h->st));
+    if (!all_ok) {
+      fprintf(stderr, "ch_comm_init: peer-memory probe failed on some rank; using NCCL\n");
+      for (void* q : h->ipc_open) cudaIpcCloseMemHandle(q);
+      h->ipc_open.clear();
+      for (int i = 0; i < A_N; ++i) h->nb_lo[i] = h->nb_hi[i] = nullptr;
+      cudaGetLastError();
+      return CH_OK;
+    }
+  }
   h->p2p = 1;
   return CH_OK;
 }

@@ -49,6 +49,10 @@ struct ZList {
 void launch_cgs_px(const Geom& g, const ZList& zl, int n, int first_block, int write_p, int need,
                    const double* T, const KScal* sc, double* P, double* X, cudaStream_t st);
 
+// peer-memory clique probe (xrank.cu): edge rows into the neighbours' ghost
+// rows + one cross-rank combine, as one multi-slab CG iteration does them
+void launch_peer_probe(const XPeers* xp, unsigned epoch, double* loc, int nloc, const Geom& g0,
+                       double* lo, const Geom& g1, double* hi, double* out, cudaStream_t st);
 void launch_cgs_delta0(const OpDesc& d, const Geom& g, const double* z, const RedArgs& ra,
                        cudaStream_t st);
 double cgs_bytes(int kind, int first, int tt);

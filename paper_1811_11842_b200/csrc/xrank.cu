@@ -58,6 +58,46 @@ __global__ void __launch_bounds__(32) k_xrank_selftest(const XPeers* xps, double
   }
 }
 
+// Probe of a freshly mapped clique (ch_comm_init, before any sweep uses it):
+// the same stores and the same combine as one multi-slab CG iteration.  Every
+// thread writes the pattern row * 1e6 + column + 0.25 of the first two rows of
+// its first slab into the lower neighbour's ghost rows and of the last two rows
+// of its last slab into the upper neighbour's (through `lo` / `hi`, offset like
+// the sweep's zlo / zhi), fences at system scope, then warp 0 runs
+// xrank_combine on the totals (r + 1) * (k + 1) of each local slab.  The
+// caller checks its own ghost rows and the sums after the kernel.
+__global__ void __launch_bounds__(256) k_peer_probe(const XPeers* xp, unsigned epoch, double* loc,
+                                                     int nloc, Geom g0, double* lo, Geom g1,
+                                                     double* hi, double* out) {
+  const int t = threadIdx.x;
+  for (int c = t; c < g0.nx; c += blockDim.x) {
+    if (lo)
+      for (int r = 0; r < 2; ++r) {
+        const int gq = g0.j0 + r;
+        lo[off(g0, gq, c)] = gq * 1e6 + c + 0.25;
+      }
+    if (hi)
+      for (int r = 0; r < 2; ++r) {
+        const int gq = g1.j0 + g1.nyl - 2 + r;
+        hi[off(g1, gq, c)] = gq * 1e6 + c + 0.25;
+      }
+  }
+  if (t < nloc * 3) loc[(t / 3) * 8 + t % 3] = (xp->rank + 1.0) * (t % 3 + 1.0);
+  __threadfence_system();
+  __syncthreads();
+  if (t < 32) {
+    double r[8];
+    const bool ok = xrank_combine<3>(xp, epoch, loc, nloc, r);
+    if (t == 0)
+      for (int k = 0; k < 3; ++k) out[k] = ok ? r[k] : -1.0;
+  }
+}
+
+void launch_peer_probe(const XPeers* xp, unsigned epoch, double* loc, int nloc, const Geom& g0,
+                       double* lo, const Geom& g1, double* hi, double* out, cudaStream_t st) {
+  k_peer_probe<<<1, 256, 0, st>>>(xp, epoch, loc, nloc, g0, lo, g1, hi, out);
+}
+
 }  // namespace chb
 
 using namespace chb;
