@@ -15,7 +15,3 @@ for c in 1 2; do
   timeout 600 python bench.py --config $c --matvec 0 > gpurun_out/bench_config$c.json 2> gpurun_out/bench_config$c.err
   echo bench_c$c=$? >> $S
 done
-for v in k6 k10 k12; do
-  CHB_LIB=$PWD/paper_1811_11842_b200/libch_b200_$v.so timeout 300 python scripts/kbench.py --solve mom_v --stride 1 > gpurun_out/kbn_$v.json 2>&1
-done
-timeout 300 python scripts/kbench.py --solve mom_v --stride 1 > gpurun_out/kbn_k8.json 2>&1
