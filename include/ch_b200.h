@@ -259,7 +259,12 @@ int ch_solve(ch_handle* h, int op, const double* b, double* x, int where);
 int ch_get_stats(const ch_handle* h, ch_stats* out);
 int ch_reset_stats(ch_handle* h);
 /* Sample every `stride`-th launch of each kernel class with a CUDA event pair
- * on the library stream (0 = off). */
+ * on the library stream (0 = off).  The CG sweeps are sampled as groups of up
+ * to 8 consecutive launches of one solve between ONE pair (kc_timed counts
+ * every launch of the group): an event between two sweeps would keep the
+ * second from starting under programmatic dependent launch, so a group times
+ * the sweeps as the chain runs them.  A group holds no p/x launch and no
+ * convergence poll. */
 int ch_enable_timing(ch_handle* h, int stride);
 
 /* Self-test of the peer-memory combine of the CG sweep on one

@@ -52,6 +52,7 @@ struct Timer {
     long iter;  // >= 0: Krylov iteration index of the launch (for useful filtering), -1: always
     double bytes;
     cudaEvent_t e0, e1;
+    int n = 1;  // launches between the two events (sweep groups: TGRP)
   };
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> pool;
@@ -184,10 +185,13 @@ struct KTime {
   bool on = false;
   cudaEvent_t e0, e1;
   // bytes: algorithmic bytes of ONE slab launch; the timed region covers all slabs
-  KTime(ch_handle* hh, int k, double b, long it = -1) : h(hh), kc(k), iter(it), bytes(b * hh->S) {
+  // count_only: launch accounting without events (the CG sweeps are timed in
+  // groups by SweepTimer)
+  KTime(ch_handle* hh, int k, double b, long it = -1, bool count_only = false)
+      : h(hh), kc(k), iter(it), bytes(b * hh->S) {
     h->stats.launches += h->S;
     h->stats.kc_launches[kc] += h->S;
-    if (h->tm.stride > 0 && (h->tm.counter[kc]++ % h->tm.stride) == 0) {
+    if (!count_only && h->tm.stride > 0 && (h->tm.counter[kc]++ % h->tm.stride) == 0) {
       on = true;
       e0 = ev_get(h);
       e1 = ev_get(h);
@@ -197,7 +201,45 @@ struct KTime {
   ~KTime() {
     if (on) {
       cudaEventRecord(e1, h->st);
-      h->tm.pending.push_back({kc, iter, bytes, e0, e1});
+      h->tm.pending.push_back({kc, iter, bytes, e0, e1, 1});
+    }
+  }
+};
+
+// CG sweeps are timed as groups of TGRP consecutive launches of one solve
+// between ONE event pair: an event recorded between two sweeps keeps the
+// second from starting under programmatic dependent launch, so a pair per
+// launch times every sampled sweep without the overlap the chain runs with.
+// A group never contains the deferred p/x launch or a convergence poll.
+constexpr int TGRP = 8;
+struct SweepTimer {
+  ch_handle* h;
+  int kc;
+  int left = 0, n = 0;
+  bool due = false;
+  double bytes = 0.0;
+  cudaEvent_t e0;
+  SweepTimer(ch_handle* hh, int k) : h(hh), kc(k) {}
+  // before sweep k (it-th of a chunk of `chunk` launches, p/x after every m-th)
+  void before(long k, int it, int chunk, int m) {
+    if (h->tm.stride <= 0 || left > 0) return;
+    if ((h->tm.counter[kc]++ % h->tm.stride) == 0) due = true;
+    const int G = m < TGRP ? m : TGRP;
+    if (due && k > 0 && it + G <= chunk && (int)(k % m) + G <= m) {
+      due = false;
+      left = n = G;
+      bytes = 0.0;
+      e0 = ev_get(h);
+      cudaEventRecord(e0, h->st);
+    }
+  }
+  void after(long k, double b) {
+    if (left == 0) return;
+    bytes += b * h->S;
+    if (--left == 0) {
+      cudaEvent_t e1 = ev_get(h);
+      cudaEventRecord(e1, h->st);
+      h->tm.pending.push_back({kc, k + 1, bytes, e0, e1, n});
     }
   }
 };
@@ -210,7 +252,7 @@ void harvest(ch_handle* h, long useful_iters) {
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, r.e0, r.e1) == cudaSuccess) {
         h->stats.kc_ms[r.kc] += ms;
-        h->stats.kc_timed[r.kc] += 1;
+        h->stats.kc_timed[r.kc] += r.n;
         h->stats.kc_bytes[r.kc] += r.bytes;
       }
     }
@@ -523,9 +565,11 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
   long k = 0;
   long npoll = 0;
   int chunk = 4;
+  SweepTimer swt(h, kc_sys);
   for (;;) {
     for (int it = 0; it < chunk; ++it, ++k) {
       const int first = (k == 0), dir = (k & 1) ? -1 : 1;
+      swt.before(k, it, chunk, m);
       const int zi = Zr[k % NZ], zo = Zr[(k + 1) % NZ];
       // three-term: the sweep reads z_{k-1} (still in the ring) instead of s_{k-1}
       // and writes no s
@@ -554,13 +598,13 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
         RedArgs ra = rargs(h, FIN_CGS, sys, 0);
         ra.xp = h->xp_dev;
         ra.epoch = ++h->epoch;
-        KTime kt(h, kc_sys, cgs_bytes(ekind, first, tt) * cells, k + 1);
+        KTime kt(h, kc_sys, cgs_bytes(ekind, first, tt) * cells, k + 1, true);
         h->stats.launches -= h->S - 1;   // one launch for all slabs
         h->stats.kc_launches[kc_sys] -= h->S - 1;
         launch_cgs_iter_ms(opdesc(h, kind, h->sl[0]), ma, first, dir, tt, ra, h->st);
       } else {
         {
-          KTime kt(h, kc_sys, cgs_bytes(ekind, first, tt) * cells, k + 1);
+          KTime kt(h, kc_sys, cgs_bytes(ekind, first, tt) * cells, k + 1, true);
           for (int s = 0; s < h->S; ++s) {
             Slab& sl = h->sl[s];
             launch_cgs_iter(opdesc(h, kind, sl), sl.g, sl.a[zi], sl.a[zo], sl.a[si],
@@ -570,6 +614,7 @@ int cgs_solve(ch_handle* h, int sys, int kind, int xid, int bid, int nullspace, 
         }
         TRY(iter_exchange(h, FIN_CGS, sys, 3, zo, so));
       }
+      swt.after(k, cgs_bytes(ekind, first, tt) * cells);
       if ((k + 1) % m == 0) TRY(px(k, m, 1));
     }
     TRY(check_launch(h, "cgs iteration"));
