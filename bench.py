@@ -222,7 +222,14 @@ def run_ours(args, rank, world, local_rank):
             "traffic_source": traffic_src,
             "peak_source": peak_kind,
             "bytes_per_launch": kd["bytes"] / max(kd["timed"], 1),
-            "avg_launch_ms": kd["ms"] / max(kd["timed"], 1)}
+            "avg_launch_ms": kd["ms"] / max(kd["timed"], 1),
+            "timing": "CUDA events on the library stream; CG sweeps sampled as groups of 8 "
+                      "consecutive launches per event pair (PDL chain intact), other classes "
+                      "per launch",
+            # consistency: sum over classes of launches x average sampled time, against the
+            # device-timed region (1.0 = the samples account for the whole step)
+            "classes_over_region": sum(v["ms"] / max(v["timed"], 1) * v["launches"]
+                                       for v in st["kernels"].values() if v["launches"]) / ms}
     per_class = {k: {"launches": v["launches"], "timed": v["timed"],
                      "avg_ms": v["ms"] / max(v["timed"], 1),
                      "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
