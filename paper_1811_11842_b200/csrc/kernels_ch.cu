@@ -22,11 +22,14 @@ namespace chb {
 // of the advection part (u on the cell's two x-faces, v on its two y-faces)
 // come straight from global memory at the thread's own columns.  Per cell:
 // read x, D^-1, phi* (+ u, v; + dot operands), write y.
+#ifndef CHB_RM_NST
+#define CHB_RM_NST 8    // ring depth (rows in flight per CTA)
+#endif
 namespace {
 constexpr int RM_T = 128;             // threads (4 warps)
 constexpr int RM_CW = 2 * RM_T;       // max columns per chunk
 constexpr int RM_SEG = RM_CW + 4;     // staged columns c0 - 2 .. c0 + wc + 1
-constexpr int RM_NST = 8;
+constexpr int RM_NST = CHB_RM_NST;
 constexpr int RM_STAGE = 3 * RM_SEG;  // x | dinv | phi*
 
 __device__ __forceinline__ int rm_fold(const Geom& g, int gj) {

@@ -41,4 +41,6 @@ for r in /tmp/prof/prof_mom_v.ncu-rep /tmp/prof/prof_poisson.ncu-rep; do
   sz=$(stat -c %s $r 2>/dev/null || echo 0)
   [ "$sz" -lt 20000000 ] && cp $r gpurun_out/
 done
+# the launch list itself (5000 launches, ~1 MB)
+cp /tmp/prof/launches_head.csv gpurun_out/ 2>/dev/null
 du -sh gpurun_out >> $S
