@@ -23,7 +23,7 @@ namespace chb {
 // come straight from global memory at the thread's own columns.  Per cell:
 // read x, D^-1, phi* (+ u, v; + dot operands), write y.
 #ifndef CHB_RM_NST
-#define CHB_RM_NST 8    // ring depth (rows in flight per CTA)
+#define CHB_RM_NST 6    // ring depth (rows in flight per CTA): 6 x 18.7 KB x 5 CTAs fit one SM
 #endif
 namespace {
 constexpr int RM_T = 128;             // threads (4 warps)
@@ -77,9 +77,10 @@ __device__ __forceinline__ void rm_tile(int b, int nb, int ncb, int nyl, int& ch
 }  // namespace
 
 #ifndef CHB_MINB_CH
-#define CHB_MINB_CH 4   // resident CTAs per SM requested from ptxas (<= 128 registers):
-                        // measured 4 vs the unconstrained 3 (149 registers): +16 % (4096^2),
-                        // +25 % (16384^2) on the isolated apply, no spills
+#define CHB_MINB_CH 5   // resident CTAs per SM requested from ptxas (<= 102 registers,
+                        // 8-48 B of spills): measured on the isolated apply 4 vs the
+                        // unconstrained 3 (149 registers) +16 % (4096^2) / +25 % (16384^2);
+                        // 5 (ring depth 6) vs 4 (depth 8) +4 % / +4 %; 6 (85 registers) -21 %
 #endif
 template <int NDOT, int PRE>
 __global__ void __launch_bounds__(RM_T, CHB_MINB_CH) k_ch_rm(Geom g, ChCoef cc, const double* __restrict__ x,
