@@ -14,7 +14,7 @@ namespace chb {
 
 // --------------------------------------------------------------------------
 // Row-marching apply: one CTA per (<= 256-column chunk x row strip), x, D^-1
-// and phi* rows streamed into an 8-deep shared-memory ring by 1-D bulk async
+// and phi* rows streamed into a 6-deep (CHB_RM_NST) shared-memory ring by 1-D bulk async
 // copies (lane 0 of warps 0-2, one array each), two columns per thread,
 // x^ = D^-1 x and w = Delta_h x^ kept in three-row register windows (w
 // recomputed on the two neighbour columns each side instead of exchanged),
