@@ -29,7 +29,12 @@ namespace {
 constexpr int RM_T = 128;             // threads (4 warps)
 constexpr int RM_CW = 2 * RM_T;       // max columns per chunk
 constexpr int RM_SEG = RM_CW + 4;     // staged columns c0 - 2 .. c0 + wc + 1
-constexpr int RM_NST = CHB_RM_NST;
+// the isolated apply (NDOT = 0) and the in-solver applies with fused dots
+// (NDOT > 0: more live registers) take their own CTAs-per-SM / ring depth
+#ifndef CHB_RM_NST_DOT
+#define CHB_RM_NST_DOT 8
+#endif
+constexpr int rm_nst(int ndot) { return ndot == 0 ? CHB_RM_NST : CHB_RM_NST_DOT; }
 constexpr int RM_STAGE = 3 * RM_SEG;  // x | dinv | phi*
 
 __device__ __forceinline__ int rm_fold(const Geom& g, int gj) {
@@ -82,16 +87,22 @@ __device__ __forceinline__ void rm_tile(int b, int nb, int ncb, int nyl, int& ch
                         // unconstrained 3 (149 registers) +16 % (4096^2) / +25 % (16384^2);
                         // 5 (ring depth 6) vs 4 (depth 8) +4 % / +4 %; 6 (85 registers) -21 %
 #endif
+#ifndef CHB_MINB_CH_DOT
+#define CHB_MINB_CH_DOT 4   // applies with fused dots: 5 CTAs/SM measured 15 % SLOWER in the
+                            // BiCGStab solve (217.7 -> 251.3 us at 4096^2): 4 stays
+#endif
+constexpr int rm_minb(int ndot) { return ndot == 0 ? CHB_MINB_CH : CHB_MINB_CH_DOT; }
 template <int NDOT, int PRE>
-__global__ void __launch_bounds__(RM_T, CHB_MINB_CH) k_ch_rm(Geom g, ChCoef cc, const double* __restrict__ x,
+__global__ void __launch_bounds__(RM_T, rm_minb(NDOT)) k_ch_rm(Geom g, ChCoef cc, const double* __restrict__ x,
                                                 double* __restrict__ y,
                                                 const double* __restrict__ d1,
                                                 const double* __restrict__ d2, int skip_done,
                                                 int skip_half, int ncb, int cw, RedArgs ra) {
   if (skip_done && ra.sc->done) return;
   if (skip_half && ra.sc->half) return;
+  constexpr int NST = NDOT == 0 ? CHB_RM_NST : CHB_RM_NST_DOT;
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t bars[RM_NST];
+  __shared__ __align__(8) uint64_t bars[NST];
   const uint32_t ring_s = s_u32(smem), bars_s = s_u32(bars);
   int chunk, jl0, jl1;
   rm_tile(blockIdx.x, gridDim.x, ncb, g.nyl, chunk, jl0, jl1);
@@ -104,20 +115,20 @@ __global__ void __launch_bounds__(RM_T, CHB_MINB_CH) k_ch_rm(Geom g, ChCoef cc, 
   const double* mysrc = warp == 0 ? x : (warp == 1 ? cc.dinv : cc.phis);
   const bool myuse = warp == 0 || warp == 2 || (warp == 1 && PRE);
   if (t == 0) {
-    for (int i = 0; i < RM_NST; ++i) mbar_init(bars + i, RM_T / 32);
+    for (int i = 0; i < NST; ++i) mbar_init(bars + i, RM_T / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (lane == 0)
-    for (int q = 0; q < RM_NST && q < nq; ++q)
+    for (int q = 0; q < NST && q < nq; ++q)
       rm_issue(g, mysrc, ring_s, bars_s, q, rbase + q, c0, wc, warp, myuse);
-  auto slot = [&](int q) { return smem + (q % RM_NST) * RM_STAGE; };
+  auto slot = [&](int q) { return smem + (q % NST) * RM_STAGE; };
   auto xh = [&](const double* st, int idx) -> double {  // x^ = D^-1 x at staged index idx
     const double v = st[idx];
     return PRE ? v * st[RM_SEG + idx] : v;
   };
   auto wait_row = [&](int q) {
-    mbar_wait_s(bars_s + 8u * (uint32_t)(q % RM_NST), (uint32_t)((q / RM_NST) & 1));
+    mbar_wait_s(bars_s + 8u * (uint32_t)(q % NST), (uint32_t)((q / NST) & 1));
   };
   // x^ rows (older -> newer) at columns c-1 .. c+2 of the thread's pair; w = Delta_h x^
   // at the pair's own columns in registers (wm, wc_, wp: rows k-1, k, k+1, indices
@@ -242,9 +253,9 @@ __global__ void __launch_bounds__(RM_T, CHB_MINB_CH) k_ch_rm(Geom g, ChCoef cc, 
       }
     }
     __syncthreads();  // ring row k - 1 consumed by every warp
-    if (lane == 0 && k >= 1 && k - 1 + RM_NST < nq) {
+    if (lane == 0 && k >= 1 && k - 1 + NST < nq) {
       fence_proxy_async();
-      rm_issue(g, mysrc, ring_s, bars_s, (k - 1) % RM_NST, rbase + k - 1 + RM_NST, c0, wc, warp,
+      rm_issue(g, mysrc, ring_s, bars_s, (k - 1) % NST, rbase + k - 1 + NST, c0, wc, warp,
                myuse);
     }
     for (int j = 0; j < 4; ++j) {
@@ -278,7 +289,7 @@ void launch_rm(const Geom& g, const ChCoef& cc, const double* x, double* y, cons
                const double* d2, int skip_done, int skip_half, const RedArgs& ra,
                cudaStream_t st) {
   auto kern = k_ch_rm<NDOT, PRE>;
-  constexpr size_t smem = (size_t)RM_NST * RM_STAGE * sizeof(double);
+  constexpr size_t smem = (size_t)rm_nst(NDOT) * RM_STAGE * sizeof(double);
   static int per_sm = -1;
   static int nsm = 0;
   if (per_sm < 0) {
